@@ -1,0 +1,416 @@
+#!/usr/bin/env python
+"""Benchmark of the QC potential sweep + GGD hot path (BASELINE.json metric:
+potential node-pairs/s, GPairs/s, at 1/2/4/8 B200).
+
+Workload (config 4 of BASELINE.json): LFR-style graph, N = 1,000,000, avg
+degree 20, unit weights, W = 10, seed 1; sigma grid log_sigma_grid(10, 32)
+(0.1W..3W, 32 points). One step = the whole sweep: the potential field of all
+rows for all 32 sigmas (row-sharded over the ranks), the all-gather of V,
+and GGD labels (successors, centers, cluster indices) for every sigma.
+One logical node-pair per sigma = one iteration of potential.cpp:32-35, so a
+step is N^2 * 32 pairs; value = N^2 * 32 / step time, whole job.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1, NCCL)
+
+--impl reference times the reference's CPU path (the oracle restatement of
+compute_potentials_parallel with all host threads; the reference itself does
+not compile here) on a bounded row sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+W_DEFAULT = 10.0
+METRIC = "potential node-pairs/s (GPairs/s)"
+UNIT = "GPairs/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["native", "reference"], default="native")
+    ap.add_argument("--workload", choices=["lfr1m", "sbm100k", "rmat22"], default="lfr1m")
+    ap.add_argument("--n-sigma", type=int, default=32)
+    ap.add_argument("--kernel", choices=["fastfwd", "replay"], default="fastfwd")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e / cpu legs)")
+    return ap.parse_args()
+
+
+def make_graph(workload):
+    from bench_tools import graphgen
+    graphgen.build()
+    if workload == "lfr1m":
+        off, nbr = graphgen.lfr()
+        desc = "LFR-style N=1e6 avg_deg~20 tau1=2.5 kmax=1000 tau2=1.5 comm=[20,1000] mu=0.3 seed=1 unit W=10"
+    elif workload == "sbm100k":
+        off, nbr = graphgen.sbm()
+        desc = "planted-partition SBM N=1e5 (100x1000) avg_deg 16 intra 0.8 seed=1 unit W=10"
+    else:
+        off, nbr = graphgen.rmat()
+        desc = "R-MAT scale 22 edge_factor 8 (0.57,0.19,0.19,0.05) seed=1 unit W=10"
+    return off, nbr, desc
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------- CPU legs
+def cpu_sample(off, nbr, sigmas, budget_s, threads):
+    """Time the oracle's compute_potentials_parallel restatement (potential.cpp:
+    18-37 per row, contiguous row blocks over `threads` threads) on a
+    deterministic row sample: every k-th row, all sigmas. Returns
+    (pairs/s, rows, elapsed, V_rows[rows][S])."""
+    from oracle import pyoracle as O
+    O.build()
+    n = len(off) - 1
+    # calibrate with one row on one thread
+    t0 = time.perf_counter()
+    O.potentials_rows(off, nbr, None, W_DEFAULT, sigmas[0], np.array([0], np.int32), workers=1)
+    per_row = max(time.perf_counter() - t0, 1e-6)
+    rows_total = max(threads, int(budget_s * threads / per_row))
+    per_sigma = max(threads, rows_total // len(sigmas))
+    per_sigma = min(per_sigma, n)
+    stride = max(1, n // per_sigma)
+    rows = np.arange(0, n, stride, dtype=np.int32)[:per_sigma]
+    out = np.empty((len(rows), len(sigmas)))
+    t0 = time.perf_counter()
+    for q, s in enumerate(sigmas):
+        out[:, q] = O.potentials_rows(off, nbr, None, W_DEFAULT, s, rows, workers=threads)
+    el = time.perf_counter() - t0
+    pairs = float(len(rows)) * n * len(sigmas)
+    return pairs / el, rows, el, out
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    off, nbr, desc = make_graph(args.workload)
+    from paper_2305_14641_b200.sweep import log_sigma_grid
+    sig = log_sigma_grid(W_DEFAULT, args.n_sigma)
+    n = len(off) - 1
+    threads = os.cpu_count() or 1
+    budget = 3.0
+    vals = []
+    rows_used = 0
+    for it in range(args.warmup + args.steps):
+        pps, rows, el, _ = cpu_sample(off, nbr, sig, budget, threads)
+        if it >= args.warmup:
+            vals.append(pps / 1e9)
+            rows_used = len(rows)
+    value = statistics.mean(vals)
+    sample = (f"{rows_used} evenly strided rows x {len(sig)} sigmas per step "
+              f"({rows_used * n * len(sig):.3e} logical pairs), oracle restatement of "
+              "compute_potentials_parallel (Eigen pexp restated, ascending-j fp64)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "n_nodes": n, "nnz": int(len(nbr)), "n_sigma": len(sig),
+                   "sigma_grid": "log_sigma_grid(10, 32)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- native arm
+def run_native(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_14641_b200 import native as N
+    from paper_2305_14641_b200 import sharded
+    from paper_2305_14641_b200.sweep import log_sigma_grid
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    N.set_kernel(N.KERNEL_FASTFWD if args.kernel == "fastfwd" else N.KERNEL_REPLAY)
+
+    off, nbr, desc = make_graph(args.workload)
+    n, nnz = len(off) - 1, len(nbr)
+    sig = np.array(log_sigma_grid(W_DEFAULT, args.n_sigma))
+    S = len(sig)
+    csr = N.Csr(off, nbr, None, W_DEFAULT)
+    dg = N.DeviceCsr(csr, dev)
+    stream = torch.cuda.Stream(dev)
+    block = sharded.row_block(n, world)
+    begin, end = sharded.row_shard(n, world, rank)
+    rows = end - begin
+
+    with torch.cuda.stream(stream):
+        shard = torch.zeros((block, S), dtype=torch.float64, device=dev)
+        full = torch.empty((world * block, S), dtype=torch.float64, device=dev) if world > 1 else None
+        succ = torch.empty((S, n), dtype=torch.int32, device=dev)
+        center = torch.empty_like(succ)
+        ci = torch.empty_like(succ)
+        nc = torch.empty(S, dtype=torch.int32, device=dev)
+        ws = torch.empty(N.dev_ggd_workspace(n, S), dtype=torch.uint8, device=dev)
+        flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 512 MiB > 126 MB L2
+    torch.cuda.synchronize(dev)
+
+    launches = [0]
+    ev = {}
+
+    def step(record=False):
+        if record:
+            ev["p0"].record(stream)
+        if rows > 0:
+            N.dev_potentials(dg, sig, begin, end, shard[:rows], stream)
+            launches[0] += N.last_launch_count()
+        if record:
+            ev["p1"].record(stream)
+        with torch.cuda.stream(stream):
+            V = sharded.gather_rows(shard, n, None, full) if world > 1 else shard[:n]
+        if record:
+            ev["p2"].record(stream)
+        N.dev_ggd(dg, V, S, succ, center, ci, nc, ws, stream)
+        launches[0] += N.last_launch_count()
+        return V
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    per_step, pot_ms, gather_ms, ggd_ms = [], [], [], []
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    launches[0] = 0
+    t_wall = time.perf_counter()
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()  # L2 flush between timed steps, outside the step's events
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        for k in ("p0", "p1", "p2"):
+            ev[k] = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(record=True)
+        e1.record(stream)
+        e1.synchronize()
+        per_step.append(e0.elapsed_time(e1))
+        pot_ms.append(ev["p0"].elapsed_time(ev["p1"]))
+        gather_ms.append(ev["p1"].elapsed_time(ev["p2"]))
+        ggd_ms.append(ev["p2"].elapsed_time(e1))
+    torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - t_wall
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    gpu_launches = launches[0]
+
+    ms = statistics.mean(per_step)
+    stats = torch.tensor([ms, statistics.mean(pot_ms), statistics.mean(gather_ms), statistics.mean(ggd_ms)],
+                         dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+    ms, pot, gat, ggd = stats.tolist()
+    pairs = float(n) * n * S
+    value = pairs / (ms / 1e3) / 1e9
+
+    # roofline of the dominant kernel (potential sweep, this rank's rows)
+    row_nnz = int(off[end] - off[begin])
+    alg_bytes = 8 * (rows + 1) + 4 * row_nnz + 8 * rows * S
+    peak, peak_kind = measured_peaks()
+    achieved = alg_bytes / (pot / 1e3) / 1e9 if pot > 0 else None
+
+    # end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        e2e = e2e_leg(args, N, torch, dist, off, nbr, sig, rank, world, dev, stream, begin, end, block)
+
+    cpu = None
+    V_host_rows = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        threads = os.cpu_count() or 1
+        pps, srows, el, vref = cpu_sample(off, nbr, sig, args.cpu_seconds, threads)
+        V_host_rows = shard[torch.from_numpy(srows.astype(np.int64)).to(dev)].cpu().numpy()
+        same = bool(np.array_equal(V_host_rows.view(np.int64), vref.view(np.int64)))
+        cpu = {"value": pps / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{len(srows)} strided rows x {S} sigmas ({len(srows) * n * S:.3e} pairs) in {el:.1f}s, "
+                         f"oracle restatement of compute_potentials_parallel; GPU rows bit-identical: {same}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "n_nodes": n, "nnz": int(nnz), "n_sigma": S,
+                       "sigma_grid": f"log_sigma_grid(10, {S})", "kernel": args.kernel,
+                       "parallelism": f"row-shard x{world} + all-gather(V)",
+                       "l2": "512 MiB write between timed steps (excluded from the per-step events)",
+                       "step": "potentials(all rows, all sigmas) + all-gather V + GGD(succ, centers, labels)"},
+            "breakdown_ms": {"potentials": pot, "allgather": gat, "ggd": ggd, "wall_s_timed_region": wall},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "kernel": "potential_kernel<FASTFWD,unit>",
+                         "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
+                         "note": "algorithmic bytes = 8(rows+1) + 4*nnz + 8*rows*S; the exact fast-forward is "
+                                 "issue-bound (fp64/int chain arithmetic), see DESIGN.md"},
+            "clocks": clocks, "gpu_launches": gpu_launches,
+            "e2e": e2e, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_leg(args, N, torch, dist, off, nbr, sig, rank, world, dev, stream, begin, end, block):
+    """Same metric through the public API with pinned host buffers: every step
+    copies the CSR host->device and the labels device->host."""
+    n, S = len(off) - 1, len(sig)
+    pin_off = torch.from_numpy(off).pin_memory()
+    pin_nbr = torch.from_numpy(nbr).pin_memory()
+    steps = max(1, min(args.steps, 3))
+    if world == 1:
+        csr = N.Csr(pin_off.numpy(), pin_nbr.numpy(), None, W_DEFAULT)
+        center = torch.empty((S, n), dtype=torch.int32).pin_memory().numpy()
+        ci = torch.empty((S, n), dtype=torch.int32).pin_memory().numpy()
+        k = np.zeros(S, np.int32)
+        sarr = np.ascontiguousarray(sig)
+        N.cluster_sweep_raw(csr, sarr, center, ci, k)  # warm-up
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            N.cluster_sweep_raw(csr, sarr, center, ci, k)  # gqc_cluster_sweep: H2D CSR, compute, D2H labels
+            times.append(time.perf_counter() - t0)
+        t = statistics.mean(times)
+        return {"value": float(n) * n * S / t / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(off.nbytes + nbr.nbytes),
+                "d2h_bytes_per_step": int(center.nbytes + ci.nbytes + k.nbytes),
+                "api": "gqc_cluster_sweep (C-ABI, host buffers)", "ms_per_step": t * 1e3}
+    # multi-GPU: per rank, H2D of the CSR, its row shard, all-gather, GGD, D2H of its rows' labels
+    from paper_2305_14641_b200 import sharded
+    rows = end - begin
+    d_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    d_nbr = torch.empty(len(nbr), dtype=torch.int32, device=dev)
+    dg = N.DeviceCsr.__new__(N.DeviceCsr)
+    dg.n, dg.nnz, dg.W, dg.offsets, dg.nbr, dg.w = n, len(nbr), W_DEFAULT, d_off, d_nbr, None
+    shard = torch.zeros((block, S), dtype=torch.float64, device=dev)
+    full = torch.empty((world * block, S), dtype=torch.float64, device=dev)
+    center = torch.empty((S, n), dtype=torch.int32, device=dev)
+    ci = torch.empty_like(center)
+    nc = torch.empty(S, dtype=torch.int32, device=dev)
+    ws = torch.empty(N.dev_ggd_workspace(n, S), dtype=torch.uint8, device=dev)
+    out_ci = torch.empty((S, max(rows, 1)), dtype=torch.int32).pin_memory()
+
+    def one():
+        with torch.cuda.stream(stream):
+            d_off.copy_(pin_off, non_blocking=True)
+            d_nbr.copy_(pin_nbr, non_blocking=True)
+            if rows > 0:
+                N.dev_potentials(dg, sig, begin, end, shard[:rows], stream)
+            V = sharded.gather_rows(shard, n, None, full)
+            N.dev_ggd(dg, V, S, None, center, ci, nc, ws, stream)
+            if rows > 0:
+                out_ci[:, :rows].copy_(ci[:, begin:end], non_blocking=True)
+        stream.synchronize()
+
+    one()
+    dist.barrier()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        one()
+        times.append(time.perf_counter() - t0)
+    t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t = float(t.item())
+    return {"value": float(n) * n * S / t / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": int(world * (off.nbytes + nbr.nbytes)),
+            "d2h_bytes_per_step": int(4 * S * n), "api": "gqc_dev_* per rank + NCCL all-gather", "ms_per_step": t * 1e3}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_native(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,140 @@
+/*
+ * gqc.h — C-ABI of the B200-native QC potential sweep + Graph Gradient Descent.
+ *
+ * This is the drop-in boundary for the reference's hot path. Each entry point
+ * replaces one graphqc C++ function (paths relative to the reference's proj/):
+ *
+ *   gqc_potentials          <- graphqc::compute_potentials / compute_potentials_parallel
+ *                              (include/graphqc/potential.hpp:33-37, src/potential.cpp:53-87),
+ *                              batched over sigma.
+ *   gqc_node_potential      <- graphqc::node_potential (potential.hpp:30, potential.cpp:46-51)
+ *   gqc_build_successors    <- graphqc::build_successors (ggd.hpp:28, ggd.cpp:7-24)
+ *   gqc_resolve_centers     <- graphqc::resolve_centers (ggd.hpp:33, ggd.cpp:26-57)
+ *   gqc_cluster_sweep       <- graphqc::cluster (ggd.hpp:37, ggd.cpp:59-62) for every sigma of a
+ *                              grid, i.e. the per-sigma loop of graphqc::run_sweep (sweep.cpp:50-57)
+ *   gqc_dev_*               <- the same operations on device-resident buffers (row-sharded
+ *                              potentials for multi-GPU; the collective lives in the host layer)
+ *
+ * Conventions: plain pointers and sizes, no C++ or torch types. Host-buffer
+ * entry points (gqc_potentials, gqc_build_successors, gqc_resolve_centers,
+ * gqc_cluster_sweep, gqc_node_potential) copy inputs to the current CUDA
+ * device and results back; the caller owns every buffer. Errors are status
+ * codes mirroring the reference's exception classes; gqc_last_error() returns
+ * the message of the calling thread's last failure (same texts as the
+ * reference, e.g. "sigma must be positive"). Calls are serialized per process.
+ * There is no CPU fallback: without a usable CUDA device every compute entry
+ * point fails with GQC_ECUDA.
+ */
+#ifndef GQC_H
+#define GQC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum gqc_status {
+    GQC_OK = 0,
+    GQC_EINVAL = 1, /* std::invalid_argument (bad sigma, size mismatch, successor out of range) */
+    GQC_ERANGE = 2, /* std::out_of_range (bad node id) */
+    GQC_ECYCLE = 3, /* std::logic_error ("successor map contains a cycle") */
+    GQC_EIO = 4,    /* graphqc::IoError */
+    GQC_ECUDA = 5,  /* CUDA runtime failure or no device */
+    GQC_ENOMEM = 6, /* device or host allocation failure (std::bad_alloc) */
+    GQC_ENCCL = 7   /* reserved for collective failures */
+} gqc_status;
+
+/* Undirected CSR exactly as graphqc::Graph stores it (graph.hpp:66-71):
+ * offsets[n+1] (int64), nbr[nnz] ascending within each row (int32),
+ * w[nnz] positive distances or NULL for unit weights, W = default distance
+ * of non-adjacent pairs. Borrowed for the duration of a call. */
+typedef struct gqc_csr {
+    int32_t n;
+    int64_t nnz;
+    const int64_t* offsets;
+    const int32_t* nbr;
+    const double* w;
+    double W;
+} gqc_csr;
+
+/* Exp provider: which exp the reference build used for exp(-d^2/2sigma^2)
+ * at potential.cpp:26. EIGEN = Eigen 3.4 pexp on SSE2 packets of two plus
+ * glibc std::exp for the N mod 2 tail element (the default Release build);
+ * GLIBC = std::exp for every element. */
+typedef enum gqc_exp_mode { GQC_EXP_EIGEN = 0, GQC_EXP_GLIBC = 1 } gqc_exp_mode;
+
+/* Potential kernel: FASTFWD = exact run fast-forward (default, O(deg + log N)
+ * per row); REPLAY = dense in-order replay (O(N) per row, the parity anchor).
+ * Both are bit-identical to the reference's ascending-j fp64 sums. */
+typedef enum gqc_kernel { GQC_KERNEL_FASTFWD = 0, GQC_KERNEL_REPLAY = 1 } gqc_kernel;
+
+typedef enum gqc_option { GQC_OPT_EXP_MODE = 1, GQC_OPT_KERNEL = 2 } gqc_option;
+
+const char* gqc_last_error(void);
+const char* gqc_version(void);
+gqc_status gqc_set_option(gqc_option key, int64_t value);
+gqc_status gqc_get_option(gqc_option key, int64_t* value);
+/* Number of CUDA devices visible (0 on a machine without a GPU). */
+int32_t gqc_device_count(void);
+
+/* ---------------------------------------------------------------- host API */
+
+/* v_out[k*n + i] = potential of node i at sigmas[k] (sigma-major, one
+ * PotentialField::values per sigma). sigma <= 0 -> GQC_EINVAL. */
+gqc_status gqc_potentials(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out);
+
+/* One node (node_potential). Bad node -> GQC_ERANGE, bad sigma -> GQC_EINVAL. */
+gqc_status gqc_node_potential(const gqc_csr* g, int32_t node, double sigma, double* out);
+
+/* succ[i] = lexicographic (v, id) argmin over {i} + neighbors(i). v has n entries. */
+gqc_status gqc_build_successors(const gqc_csr* g, const double* v, int32_t* succ);
+
+/* Chase succ to fixed points. Out-of-range successor -> GQC_EINVAL
+ * ("successor id out of range"), cycle -> GQC_ECYCLE ("successor map contains
+ * a cycle"), reporting whichever the reference's ascending chase meets first.
+ * cluster_index numbers centers densely by ascending center id. */
+gqc_status gqc_resolve_centers(int32_t n, const int32_t* succ, int32_t* center, int32_t* cluster_index,
+                               int32_t* num_clusters);
+
+/* Full pipeline per sigma (potentials -> successors -> centers). Outputs are
+ * sigma-major [n_sigma][n]; v_out and succ_out may be NULL. num_clusters_out
+ * has n_sigma entries. */
+gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out,
+                             int32_t* succ_out, int32_t* center_out, int32_t* cluster_index_out,
+                             int32_t* num_clusters_out);
+
+/* -------------------------------------------------------------- device API */
+/* All pointers in gqc_csr and the buffers below are device pointers on the
+ * current device; `stream` is a cudaStream_t (NULL = legacy default stream).
+ * sigmas stays a host array (the per-sigma exp constants are a host concern).
+ * Nothing is synchronized: errors from the kernels surface at the caller's
+ * next synchronization. */
+
+/* Potentials of rows [row_begin, row_end) for all sigmas, node-major:
+ * v_rows[(i - row_begin) * n_sigma + k]. Row shards of a multi-GPU sweep. */
+gqc_status gqc_dev_potentials(const gqc_csr* g, const double* sigmas, int32_t n_sigma, int32_t row_begin,
+                              int32_t row_end, double* v_rows, void* stream);
+
+/* Scratch bytes gqc_dev_ggd needs for n nodes and n_sigma sigmas. */
+size_t gqc_dev_ggd_workspace(int32_t n, int32_t n_sigma);
+
+/* GGD for all sigmas from a node-major potential matrix v[n][n_sigma]:
+ * sigma-major succ/center/cluster_index [n_sigma][n] and num_clusters[n_sigma]
+ * (all device). succ may be NULL. */
+gqc_status gqc_dev_ggd(const gqc_csr* g, const double* v, int32_t n_sigma, int32_t* succ, int32_t* center,
+                       int32_t* cluster_index, int32_t* num_clusters, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
+/* Node-major [n][n_sigma] -> sigma-major [n_sigma][n] transpose (device). */
+gqc_status gqc_dev_transpose(const double* v_nm, int32_t n, int32_t n_sigma, double* v_sm, void* stream);
+
+/* Number of kernel launches the last gqc_* call issued (for launch accounting). */
+int64_t gqc_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GQC_H */

@@ -1,0 +1,473 @@
+// C-ABI of libgqc (include/gqc.h): validation with the reference's error
+// semantics, per-sigma constants from the host exp provider, device buffer
+// cache, host<->device staging, and orchestration of the kernels in
+// kernels.cu. No CPU compute path exists: without a CUDA device every compute
+// entry point fails with GQC_ECUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <new>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/gqc.h"
+#include "gqc_internal.h"
+
+namespace gqc {
+
+namespace {
+
+thread_local std::string t_err;
+thread_local long long t_launches = 0;
+std::mutex g_mu;  // calls are serialized per process
+
+struct Options {
+    int exp_mode = GQC_EXP_EIGEN;
+    int kernel = GQC_KERNEL_FASTFWD;
+} g_opt;
+
+struct Fail {
+    gqc_status st;
+    std::string msg;
+};
+
+[[noreturn]] void fail(gqc_status st, const std::string& msg) { throw Fail{st, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    if (e == cudaErrorMemoryAllocation) fail(GQC_ENOMEM, std::string(what) + ": " + cudaGetErrorString(e));
+    fail(GQC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void cuda_check(int e, const char* what) { cuda_check(static_cast<cudaError_t>(e), what); }
+
+template <class F>
+gqc_status guarded(F&& f) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    t_launches = 0;
+    try {
+        f();
+        return GQC_OK;
+    } catch (const Fail& e) {
+        t_err = e.msg;
+        return e.st;
+    } catch (const std::bad_alloc&) {
+        t_err = "allocation failure";
+        return GQC_ENOMEM;
+    } catch (const std::exception& e) {
+        t_err = e.what();
+        return GQC_ECUDA;
+    }
+}
+
+// Grow-only device buffers, one set per device: repeated calls reuse memory.
+struct DevBuf {
+    void* p = nullptr;
+    std::size_t cap = 0;
+    template <class T>
+    T* get(std::size_t count) {
+        const std::size_t bytes = std::max<std::size_t>(count * sizeof(T), 256);
+        if (bytes > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+            cap = bytes;
+        }
+        return static_cast<T*>(p);
+    }
+};
+
+struct DeviceCtx {
+    cudaStream_t stream = nullptr;
+    DevBuf off, nbr, w, v_nm, v_sm, succ, center, ci, nc, ws, tail, entry;
+};
+
+DeviceCtx& ctx() {
+    static std::map<int, DeviceCtx> all;
+    int dev = 0;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        fail(GQC_ECUDA, "no CUDA device available (libgqc has no CPU path)");
+    }
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    DeviceCtx& c = all[dev];
+    if (!c.stream) cuda_check(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    return c;
+}
+
+void check_csr_shape(const gqc_csr* g) {
+    if (!g) fail(GQC_EINVAL, "graph is null");
+    if (g->n < 1) fail(GQC_EINVAL, "graph needs at least one node");  // graph.cpp:28
+    if (g->nnz < 0) fail(GQC_EINVAL, "negative edge count");
+    if (!g->offsets || (g->nnz > 0 && !g->nbr)) fail(GQC_EINVAL, "graph arrays are null");
+    if (!(g->W > 0.0)) fail(GQC_EINVAL, "default distance must be positive");  // graph.cpp:29
+}
+
+void check_sigmas(const double* sigmas, int n_sigma) {
+    if (n_sigma < 1 || !sigmas) fail(GQC_EINVAL, "sigma grid is empty");
+    for (int k = 0; k < n_sigma; ++k)
+        if (!(sigmas[k] > 0.0)) fail(GQC_EINVAL, "sigma must be positive");  // potential.cpp:39-42
+}
+
+bool all_unit(const double* w, long long nnz) {
+    for (long long k = 0; k < nnz; ++k)
+        if (w[k] != 1.0) return false;
+    return true;
+}
+
+// Weight information the potential launches need from the host side.
+struct HostWeights {
+    const double* w = nullptr;  // host weights (nnz) or nullptr
+    std::vector<double> last_row_w;
+};
+
+// glibc exp over a [count][S] block, split across host threads.
+void host_exp_table(const double* d2, long long count, const std::vector<double>& neg_inv, int S, double* out) {
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const long long per = (count + hw - 1) / hw;
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < hw; ++t) {
+        const long long b = t * per, e = std::min(count, b + per);
+        if (b >= e) break;
+        pool.emplace_back([=, &neg_inv] {
+            for (long long k = b; k < e; ++k)
+                for (int s = 0; s < S; ++s) out[k * S + s] = host_glibc_exp(neg_inv[s] * d2[k]);
+        });
+    }
+    for (auto& th : pool) th.join();
+}
+
+// Potentials of rows [row_begin, row_end) into v_nm[(i-row_begin)*S + s]
+// (device), for a device-resident CSR. host_w: the same weights on the host
+// (only consulted for weighted graphs), or nullptr to fetch what is needed.
+void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S, int row_begin, int row_end,
+                    double* v_nm, const double* host_w, cudaStream_t st) {
+    const int n = g.n;
+    const int mode = g_opt.exp_mode;
+    const bool weighted = g.w != nullptr;
+    const bool tail = (mode == GQC_EXP_EIGEN) && (n % 2 == 1);
+
+    // weighted graphs: the glibc-evaluated entries the device cannot produce
+    std::vector<double> last_w;        // weights of row n-1 (Eigen tail)
+    std::vector<double> all_d2;        // d2 per entry (glibc mode)
+    long long last_beg = 0, last_deg = 0;
+    if (weighted && tail) {
+        long long o[2];
+        cuda_check(cudaMemcpy(o, g.offsets + (n - 1), 2 * sizeof(long long), cudaMemcpyDeviceToHost), "copy offsets");
+        last_beg = o[0];
+        last_deg = o[1] - o[0];
+        last_w.resize(last_deg);
+        if (last_deg > 0) {
+            if (host_w)
+                std::copy(host_w + last_beg, host_w + last_beg + last_deg, last_w.begin());
+            else
+                cuda_check(cudaMemcpy(last_w.data(), g.w + last_beg, last_deg * sizeof(double), cudaMemcpyDeviceToHost),
+                           "copy weights");
+        }
+    }
+    if (weighted && mode == GQC_EXP_GLIBC) {
+        all_d2.resize(g.nnz);
+        std::vector<double> tmp;
+        const double* hw = host_w;
+        if (!hw) {
+            tmp.resize(g.nnz);
+            if (g.nnz)
+                cuda_check(cudaMemcpy(tmp.data(), g.w, g.nnz * sizeof(double), cudaMemcpyDeviceToHost), "copy weights");
+            hw = tmp.data();
+        }
+        for (long long k = 0; k < g.nnz; ++k) all_d2[k] = hw[k] * hw[k];
+    }
+
+    for (int s0 = 0; s0 < S; s0 += kMaxSigmaPerLaunch) {
+        const int Sc = std::min(kMaxSigmaPerLaunch, S - s0);
+        PotentialLaunch P{};
+        P.n = n;
+        P.n_sigma = Sc;
+        P.row_begin = row_begin;
+        P.row_end = row_end;
+        P.offsets = g.offsets;
+        P.nbr = g.nbr;
+        P.w = g.w;
+        P.w2 = g.W * g.W;
+        P.tail = tail ? 1 : 0;
+        P.out = v_nm;
+        P.out_ld = S;
+        P.out_col0 = s0;
+        std::vector<double> neg_inv(Sc);
+        for (int s = 0; s < Sc; ++s) {
+            P.c[s] = make_sigma_consts(sigmas[s0 + s], g.W, mode);
+            neg_inv[s] = P.c[s].neg_inv;
+        }
+        if (!weighted) {
+            P.weight_mode = kUnit;
+        } else if (mode == GQC_EXP_EIGEN) {
+            P.weight_mode = kDevicePexp;
+            if (tail && last_deg > 0) {
+                std::vector<double> d2(last_deg), tab(last_deg * Sc);
+                for (long long q = 0; q < last_deg; ++q) d2[q] = last_w[q] * last_w[q];
+                host_exp_table(d2.data(), last_deg, neg_inv, Sc, tab.data());
+                double* dtab = C.tail.get<double>(tab.size());
+                cuda_check(cudaMemcpyAsync(dtab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, st),
+                           "copy tail table");
+                cuda_check(cudaStreamSynchronize(st), "sync");  // tab is a local
+                P.tail_exp = dtab;
+            }
+        } else {
+            P.weight_mode = kEntryTable;
+            std::vector<double> tab(static_cast<std::size_t>(g.nnz) * Sc);
+            host_exp_table(all_d2.data(), g.nnz, neg_inv, Sc, tab.data());
+            double* dtab = C.entry.get<double>(std::max<std::size_t>(tab.size(), 1));
+            if (!tab.empty())
+                cuda_check(cudaMemcpyAsync(dtab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, st),
+                           "copy entry table");
+            cuda_check(cudaStreamSynchronize(st), "sync");
+            P.entry_exp = dtab;
+            P.entry_ld = Sc;
+            P.entry_col0 = 0;
+        }
+        cuda_check(launch_potentials(P, g_opt.kernel, st), "potential kernel launch");
+    }
+}
+
+// Device copy of a host CSR (cached buffers). Unit weights are detected and
+// passed as NULL so the constant-only kernel runs.
+gqc_csr upload_csr(DeviceCtx& C, const gqc_csr* g, cudaStream_t st, const double** host_w_out) {
+    const long long nnz = g->nnz;
+    if (g->offsets[0] != 0 || g->offsets[g->n] != nnz) fail(GQC_EINVAL, "CSR offsets do not match nnz");
+    gqc_csr d = *g;
+    auto* off = C.off.get<std::int64_t>(g->n + 1);
+    auto* nbr = C.nbr.get<std::int32_t>(std::max<long long>(nnz, 1));
+    cuda_check(cudaMemcpyAsync(off, g->offsets, (g->n + 1) * sizeof(std::int64_t), cudaMemcpyHostToDevice, st),
+               "copy offsets");
+    if (nnz)
+        cuda_check(cudaMemcpyAsync(nbr, g->nbr, nnz * sizeof(std::int32_t), cudaMemcpyHostToDevice, st), "copy nbr");
+    d.offsets = off;
+    d.nbr = nbr;
+    d.w = nullptr;
+    *host_w_out = nullptr;
+    if (g->w && !all_unit(g->w, nnz)) {
+        auto* w = C.w.get<double>(std::max<long long>(nnz, 1));
+        cuda_check(cudaMemcpyAsync(w, g->w, nnz * sizeof(double), cudaMemcpyHostToDevice, st), "copy weights");
+        d.w = w;
+        *host_w_out = g->w;
+    }
+    return d;
+}
+
+}  // namespace
+
+void count_launch(int k) { t_launches += k; }
+
+}  // namespace gqc
+
+using namespace gqc;
+
+extern "C" {
+
+const char* gqc_last_error(void) { return t_err.c_str(); }
+const char* gqc_version(void) { return "gqc 0.1 sm_100a"; }
+int64_t gqc_last_launch_count(void) { return t_launches; }
+
+int32_t gqc_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return c;
+}
+
+gqc_status gqc_set_option(gqc_option key, int64_t value) {
+    return guarded([&] {
+        if (key == GQC_OPT_EXP_MODE) {
+            if (value != GQC_EXP_EIGEN && value != GQC_EXP_GLIBC) fail(GQC_EINVAL, "unknown exp mode");
+            g_opt.exp_mode = static_cast<int>(value);
+        } else if (key == GQC_OPT_KERNEL) {
+            if (value != GQC_KERNEL_FASTFWD && value != GQC_KERNEL_REPLAY) fail(GQC_EINVAL, "unknown kernel");
+            g_opt.kernel = static_cast<int>(value);
+        } else {
+            fail(GQC_EINVAL, "unknown option");
+        }
+    });
+}
+
+gqc_status gqc_get_option(gqc_option key, int64_t* value) {
+    return guarded([&] {
+        if (!value) fail(GQC_EINVAL, "null output");
+        if (key == GQC_OPT_EXP_MODE) *value = g_opt.exp_mode;
+        else if (key == GQC_OPT_KERNEL) *value = g_opt.kernel;
+        else fail(GQC_EINVAL, "unknown option");
+    });
+}
+
+gqc_status gqc_potentials(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out) {
+    return guarded([&] {
+        check_sigmas(sigmas, n_sigma);
+        check_csr_shape(g);
+        if (!v_out) fail(GQC_EINVAL, "null output");
+        DeviceCtx& C = ctx();
+        cudaStream_t st = C.stream;
+        const double* hw = nullptr;
+        gqc_csr d = upload_csr(C, g, st, &hw);
+        const std::size_t cells = static_cast<std::size_t>(g->n) * n_sigma;
+        double* v_nm = C.v_nm.get<double>(cells);
+        run_potentials(C, d, sigmas, n_sigma, 0, g->n, v_nm, hw, st);
+        double* src = v_nm;
+        if (n_sigma > 1) {
+            src = C.v_sm.get<double>(cells);
+            cuda_check(launch_transpose(v_nm, g->n, n_sigma, src, st), "transpose");
+        }
+        cuda_check(cudaMemcpyAsync(v_out, src, cells * sizeof(double), cudaMemcpyDeviceToHost, st), "copy V");
+        cuda_check(cudaStreamSynchronize(st), "potential sweep");
+    });
+}
+
+gqc_status gqc_node_potential(const gqc_csr* g, int32_t node, double sigma, double* out) {
+    return guarded([&] {
+        check_sigmas(&sigma, 1);  // potential.cpp:47 checks sigma before the node
+        check_csr_shape(g);
+        if (node < 0 || node >= g->n) fail(GQC_ERANGE, "node id " + std::to_string(node) + " out of range");
+        if (!out) fail(GQC_EINVAL, "null output");
+        DeviceCtx& C = ctx();
+        cudaStream_t st = C.stream;
+        const double* hw = nullptr;
+        gqc_csr d = upload_csr(C, g, st, &hw);
+        double* v = C.v_nm.get<double>(1);
+        run_potentials(C, d, &sigma, 1, node, node + 1, v, hw, st);
+        cuda_check(cudaMemcpyAsync(out, v, sizeof(double), cudaMemcpyDeviceToHost, st), "copy V");
+        cuda_check(cudaStreamSynchronize(st), "node potential");
+    });
+}
+
+gqc_status gqc_build_successors(const gqc_csr* g, const double* v, int32_t* succ) {
+    return guarded([&] {
+        check_csr_shape(g);
+        if (!v || !succ) fail(GQC_EINVAL, "null buffer");
+        DeviceCtx& C = ctx();
+        cudaStream_t st = C.stream;
+        const double* hw = nullptr;
+        gqc_csr d = upload_csr(C, g, st, &hw);
+        double* dv = C.v_nm.get<double>(g->n);
+        int* ds = C.succ.get<int>(g->n);
+        cuda_check(cudaMemcpyAsync(dv, v, g->n * sizeof(double), cudaMemcpyHostToDevice, st), "copy V");
+        cuda_check(launch_successors(g->n, d.offsets, d.nbr, dv, 1, ds, st), "successor kernel");
+        cuda_check(cudaMemcpyAsync(succ, ds, g->n * sizeof(int), cudaMemcpyDeviceToHost, st), "copy succ");
+        cuda_check(cudaStreamSynchronize(st), "build successors");
+    });
+}
+
+gqc_status gqc_resolve_centers(int32_t n, const int32_t* succ, int32_t* center, int32_t* cluster_index,
+                               int32_t* num_clusters) {
+    return guarded([&] {
+        if (n < 0) fail(GQC_EINVAL, "negative size");
+        if (n == 0) {
+            if (num_clusters) *num_clusters = 0;
+            return;
+        }
+        if (!succ || !center || !cluster_index || !num_clusters) fail(GQC_EINVAL, "null buffer");
+        DeviceCtx& C = ctx();
+        cudaStream_t st = C.stream;
+        int* ds = C.succ.get<int>(n);
+        int* dc = C.center.get<int>(n);
+        int* dci = C.ci.get<int>(n);
+        cuda_check(cudaMemcpyAsync(ds, succ, n * sizeof(int), cudaMemcpyHostToDevice, st), "copy succ");
+        int err = 0;
+        int k = 0;
+        cuda_check(resolve_checked(n, ds, dc, dci, &k, &err, st), "resolve centers");
+        if (err == 1) fail(GQC_EINVAL, "successor id out of range");  // ggd.cpp:37-38
+        if (err == 2) fail(GQC_ECYCLE, "successor map contains a cycle");  // ggd.cpp:41
+        cuda_check(cudaMemcpyAsync(center, dc, n * sizeof(int), cudaMemcpyDeviceToHost, st), "copy center");
+        cuda_check(cudaMemcpyAsync(cluster_index, dci, n * sizeof(int), cudaMemcpyDeviceToHost, st), "copy index");
+        cuda_check(cudaStreamSynchronize(st), "resolve centers");
+        *num_clusters = k;
+    });
+}
+
+gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out,
+                             int32_t* succ_out, int32_t* center_out, int32_t* cluster_index_out,
+                             int32_t* num_clusters_out) {
+    return guarded([&] {
+        check_sigmas(sigmas, n_sigma);
+        check_csr_shape(g);
+        if (!center_out || !cluster_index_out || !num_clusters_out) fail(GQC_EINVAL, "null output");
+        DeviceCtx& C = ctx();
+        cudaStream_t st = C.stream;
+        const double* hw = nullptr;
+        gqc_csr d = upload_csr(C, g, st, &hw);
+        const int n = g->n;
+        const std::size_t cells = static_cast<std::size_t>(n) * n_sigma;
+        double* v_nm = C.v_nm.get<double>(cells);
+        run_potentials(C, d, sigmas, n_sigma, 0, n, v_nm, hw, st);
+        int* ds = C.succ.get<int>(cells);
+        int* dc = C.center.get<int>(cells);
+        int* dci = C.ci.get<int>(cells);
+        int* dnc = C.nc.get<int>(n_sigma);
+        const std::size_t wsb = labels_workspace_bytes(n, n_sigma);
+        void* ws = C.ws.get<char>(wsb);
+        cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, ds, st), "successor kernel");
+        cuda_check(launch_chase(n, n_sigma, ds, dc, st), "chase kernel");
+        cuda_check(launch_labels(n, n_sigma, dc, dci, dnc, ws, wsb, st), "label kernels");
+        if (v_out) {
+            double* src = v_nm;
+            if (n_sigma > 1) {
+                src = C.v_sm.get<double>(cells);
+                cuda_check(launch_transpose(v_nm, n, n_sigma, src, st), "transpose");
+            }
+            cuda_check(cudaMemcpyAsync(v_out, src, cells * sizeof(double), cudaMemcpyDeviceToHost, st), "copy V");
+        }
+        if (succ_out) cuda_check(cudaMemcpyAsync(succ_out, ds, cells * sizeof(int), cudaMemcpyDeviceToHost, st), "copy");
+        cuda_check(cudaMemcpyAsync(center_out, dc, cells * sizeof(int), cudaMemcpyDeviceToHost, st), "copy center");
+        cuda_check(cudaMemcpyAsync(cluster_index_out, dci, cells * sizeof(int), cudaMemcpyDeviceToHost, st), "copy");
+        cuda_check(cudaMemcpyAsync(num_clusters_out, dnc, n_sigma * sizeof(int), cudaMemcpyDeviceToHost, st), "copy");
+        cuda_check(cudaStreamSynchronize(st), "cluster sweep");
+    });
+}
+
+gqc_status gqc_dev_potentials(const gqc_csr* g, const double* sigmas, int32_t n_sigma, int32_t row_begin,
+                              int32_t row_end, double* v_rows, void* stream) {
+    return guarded([&] {
+        check_sigmas(sigmas, n_sigma);
+        check_csr_shape(g);
+        if (row_begin < 0 || row_end > g->n || row_begin > row_end) fail(GQC_ERANGE, "row range out of range");
+        if (!v_rows && row_end > row_begin) fail(GQC_EINVAL, "null output");
+        DeviceCtx& C = ctx();
+        run_potentials(C, *g, sigmas, n_sigma, row_begin, row_end, v_rows, nullptr, static_cast<cudaStream_t>(stream));
+    });
+}
+
+size_t gqc_dev_ggd_workspace(int32_t n, int32_t n_sigma) {
+    if (n < 1 || n_sigma < 1) return 0;
+    return labels_workspace_bytes(n, n_sigma);
+}
+
+gqc_status gqc_dev_ggd(const gqc_csr* g, const double* v, int32_t n_sigma, int32_t* succ, int32_t* center,
+                       int32_t* cluster_index, int32_t* num_clusters, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+    return guarded([&] {
+        check_csr_shape(g);
+        if (n_sigma < 1) fail(GQC_EINVAL, "sigma grid is empty");
+        if (!v || !center || !cluster_index || !num_clusters || !workspace) fail(GQC_EINVAL, "null buffer");
+        if (workspace_bytes < labels_workspace_bytes(g->n, n_sigma)) fail(GQC_EINVAL, "workspace too small");
+        auto st = static_cast<cudaStream_t>(stream);
+        int* s = succ ? succ : center;  // the chase runs in place on center
+        cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, s, st), "successor kernel");
+        cuda_check(launch_chase(g->n, n_sigma, s, center, st), "chase kernel");
+        cuda_check(launch_labels(g->n, n_sigma, center, cluster_index, num_clusters, workspace, workspace_bytes, st),
+                   "label kernels");
+    });
+}
+
+gqc_status gqc_dev_transpose(const double* v_nm, int32_t n, int32_t n_sigma, double* v_sm, void* stream) {
+    return guarded([&] {
+        if (n < 0 || n_sigma < 1 || !v_nm || !v_sm) fail(GQC_EINVAL, "bad transpose arguments");
+        cuda_check(launch_transpose(v_nm, n, n_sigma, v_sm, stream), "transpose");
+    });
+}
+
+}  // extern "C"

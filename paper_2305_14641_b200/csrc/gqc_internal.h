@@ -1,0 +1,70 @@
+// Internal shared definitions of libgqc (not part of the C-ABI).
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+namespace gqc {
+
+// Per-sigma constants handed to the potential kernels. "t" variants are the
+// glibc values for the reference's scalar tail column (j = N-1 when N is odd
+// in the Eigen build, potential.cpp:26).
+struct SigmaConsts {
+    double inv, neg_inv;
+    double eW, pW;    // non-adjacent pair: exp(-inv*W^2), W^2*exp(...)
+    double e1, p1;    // unit-weight neighbour
+    double eWt, pWt;  // tail column, non-adjacent
+    double e1t, p1t;  // tail column, unit-weight neighbour
+};
+constexpr int kSigmaFields = 10;
+constexpr int kMaxSigmaPerLaunch = 32;
+
+double host_pexp(double x);
+double host_glibc_exp(double x);
+double inv_two_sigma_sq(double sigma);
+SigmaConsts make_sigma_consts(double sigma, double W, int exp_mode);
+
+// Weight handling of a potential launch.
+enum WeightMode : int {
+    kUnit = 0,        // all neighbour weights 1.0: constants only
+    kDevicePexp = 1,  // per-entry device pexp (Eigen mode), tail entries from tail_exp
+    kEntryTable = 2,  // per-entry exp values precomputed on the host (glibc mode)
+};
+
+struct PotentialLaunch {
+    std::int32_t n;
+    std::int32_t n_sigma;      // sigmas in this launch (<= kMaxSigmaPerLaunch)
+    std::int32_t row_begin, row_end;
+    const std::int64_t* offsets;
+    const std::int32_t* nbr;
+    const double* w;           // nullptr for unit weights
+    double w2;                 // W*W
+    int tail;                  // column n-1 uses the glibc tail constants
+    int weight_mode;
+    const double* entry_exp;   // kEntryTable: [nnz][entry_ld] at column entry_col0 + s
+    std::int32_t entry_ld, entry_col0;
+    const double* tail_exp;    // kDevicePexp && tail: [deg(n-1)][n_sigma] glibc exp of row n-1's entries
+    double* out;               // out[(i - row_begin) * out_ld + out_col0 + s]
+    std::int32_t out_ld, out_col0;
+    SigmaConsts c[kMaxSigmaPerLaunch];
+};
+
+// Kernel launchers (kernels.cu). Return a cudaError_t as int.
+int launch_potentials(const PotentialLaunch& p, int kernel, void* stream);
+int launch_successors(std::int32_t n, const std::int64_t* offsets, const std::int32_t* nbr, const double* v,
+                      std::int32_t n_sigma, std::int32_t* succ_sm, void* stream);
+int launch_chase(std::int32_t n, std::int32_t n_sigma, const std::int32_t* succ_sm, std::int32_t* center_sm,
+                 void* stream);
+int launch_labels(std::int32_t n, std::int32_t n_sigma, const std::int32_t* center_sm, std::int32_t* cluster_index_sm,
+                  std::int32_t* num_clusters, void* workspace, std::size_t ws_bytes, void* stream);
+std::size_t labels_workspace_bytes(std::int32_t n, std::int32_t n_sigma);
+int launch_transpose(const double* v_nm, std::int32_t n, std::int32_t n_sigma, double* v_sm, void* stream);
+// Checked resolve for arbitrary successor maps: writes center/cluster_index,
+// returns status via *err_kind (0 ok, 1 out of range, 2 cycle) on the host.
+int resolve_checked(std::int32_t n, const std::int32_t* succ_dev, std::int32_t* center_dev,
+                    std::int32_t* cluster_index_dev, std::int32_t* num_clusters_host, int* err_kind, void* stream);
+
+// Launch accounting (kernels issued by the last C-ABI call).
+void count_launch(int k = 1);
+
+}  // namespace gqc

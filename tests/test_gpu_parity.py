@@ -1,0 +1,272 @@
+"""GPU parity: the sm_100a path, called through the C-ABI (libgqc.so), against
+the CPU oracle on the same seeded inputs. Integer outputs (successors,
+centers, cluster indices, counts) and the fp64 potentials are compared BIT
+FOR BIT: the reference's labels on unit-weight graphs depend on the last bit
+of the ascending-j sums, so the only tolerance is zero."""
+import numpy as np
+import pytest
+
+from oracle import pyoracle as O
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+N = pytest.importorskip("paper_2305_14641_b200.native")
+
+KERNELS = [N.KERNEL_FASTFWD, N.KERNEL_REPLAY]
+MODES = [N.EXP_EIGEN, N.EXP_GLIBC]
+
+
+@pytest.fixture(autouse=True)
+def _reset():
+    yield
+    N.set_exp_mode(N.EXP_EIGEN)
+    N.set_kernel(N.KERNEL_FASTFWD)
+
+
+def setup(kernel, mode):
+    N.set_kernel(kernel)
+    N.set_exp_mode(mode)
+
+
+def oracle_field(g, sigma, mode):
+    return O.potentials(g.offsets, g.nbr, g.wt, g.W, sigma, workers=4, mode=mode)
+
+
+def assert_bits(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    assert a.shape == b.shape
+    bad = np.flatnonzero(a.view(np.int64) != b.view(np.int64))
+    assert bad.size == 0, f"{bad.size} mismatches, first at {bad[:5]}: {a.ravel()[bad[:5]]} vs {b.ravel()[bad[:5]]}"
+
+
+SIGMAS = [0.05, 0.3, 1.0, 1.7, 2.3, 5.0, 30.0, 500.0]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("mode", MODES)
+def test_karate_potentials_bitwise(kernel, mode):
+    setup(kernel, mode)
+    g, names, lab, k = H.karate()
+    grid = O.log_sigma_grid(10.0)
+    sig = np.concatenate([grid, SIGMAS])
+    sig.sort()
+    got = N.potentials(g.csr(N), sig)
+    for q, s in enumerate(sig):
+        assert_bits(got[q], oracle_field(g, s, mode))
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("n", [2, 3, 37, 200, 257])
+@pytest.mark.parametrize("unit", [True, False])
+def test_random_graph_potentials_bitwise(kernel, mode, n, unit):
+    # oracles::random_graph shapes (odd and even N: the Eigen tail column)
+    setup(kernel, mode)
+    g = H.random_graph(n, 4.0, seed=1000 + n, unit=unit)
+    got = N.potentials(g.csr(N), SIGMAS)
+    for q, s in enumerate(SIGMAS):
+        assert_bits(got[q], oracle_field(g, s, mode))
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_structured_graphs_bitwise(kernel):
+    # stars, paths, complete graphs (long coalesced neighbour runs), planted partitions
+    setup(kernel, N.EXP_EIGEN)
+    graphs = [H.star(8), H.star(9), H.path(50), H.path(51), H.complete(33), H.complete(64),
+              H.planted(4, 32, 0.3, 0.02, seed=1), H.planted(5, 31, 0.3, 0.02, seed=2)]
+    for g in graphs:
+        got = N.potentials(g.csr(N), SIGMAS)
+        for q, s in enumerate(SIGMAS):
+            assert_bits(got[q], oracle_field(g, s, N.EXP_EIGEN))
+
+
+def test_weights_stored_as_ones_equal_unit():
+    g = H.random_graph(101, 5.0, seed=5, unit=True)
+    a = N.potentials(g.csr(N, unit_as_null=False), SIGMAS)
+    b = N.potentials(g.csr(N, unit_as_null=True), SIGMAS)
+    assert_bits(a, b)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_fastfwd_equals_replay_medium(mode):
+    # N=4001 unit SBM-like graph, many sigmas including the underflow regime
+    g = H.random_graph(4001, 16.0, seed=77, unit=True)
+    sig = np.array(sorted(set(O.log_sigma_grid(10.0, 32).tolist() + [0.05, 0.2, 0.5])))
+    N.set_exp_mode(mode)
+    N.set_kernel(N.KERNEL_REPLAY)
+    a = N.potentials(g.csr(N), sig)
+    N.set_kernel(N.KERNEL_FASTFWD)
+    b = N.potentials(g.csr(N), sig)
+    assert_bits(a, b)
+    rows = np.arange(0, g.n, 97, dtype=np.int32)
+    for q in (0, 7, 15, 31):
+        ref = O.potentials_rows(g.offsets, g.nbr, g.wt, g.W, sig[q], rows, workers=8, mode=mode)
+        assert_bits(b[q][rows], ref)
+
+
+def test_sbm_100k_fastfwd_vs_replay_and_sampled_oracle():
+    off, nbr = H.sbm_csr()
+    csr = N.Csr(off, nbr, None, 10.0)
+    sig = np.array([1.0, 2.2727, 5.0, 30.0])
+    N.set_kernel(N.KERNEL_FASTFWD)
+    b = N.potentials(csr, sig)
+    N.set_kernel(N.KERNEL_REPLAY)
+    a = N.potentials(csr, sig)
+    assert_bits(a, b)
+    rows = np.arange(0, csr.n, 1999, dtype=np.int32)
+    for q, s in enumerate(sig):
+        ref = O.potentials_rows(off, nbr, None, 10.0, s, rows, workers=8)
+        assert_bits(b[q][rows], ref)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_node_potential_and_errors(kernel):
+    setup(kernel, N.EXP_EIGEN)
+    g = H.random_graph(31, 4.0, seed=9)
+    full = N.compute_potentials(g.csr(N), 1.3)
+    for i in (0, 15, 30):
+        assert N.node_potential(g.csr(N), i, 1.3) == full[i]
+    with pytest.raises(ValueError, match="sigma must be positive"):
+        N.node_potential(g.csr(N), 0, 0.0)
+    with pytest.raises(ValueError, match="sigma must be positive"):
+        N.compute_potentials(g.csr(N), -2.0)
+    with pytest.raises(ValueError, match="workers must be at least 1"):
+        N.compute_potentials_parallel(g.csr(N), 1.0, 0)
+    with pytest.raises(IndexError, match="out of range"):
+        N.node_potential(g.csr(N), 31, 1.0)
+
+
+def test_single_node_graph():
+    g = H.G(1, np.zeros(0, np.int32), np.zeros(0, np.int32))
+    assert N.node_potential(g.csr(N), 0, 1.0) == 0.0
+    res = N.cluster(g.csr(N), 1.0)
+    assert res.num_clusters == 1 and res.center.tolist() == [0]
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_karate_labels_and_report(mode):
+    setup(N.KERNEL_FASTFWD, mode)
+    g, names, lab, k = H.karate()
+    res = N.cluster(g.csr(N), 5.0)
+    assert res.num_clusters == 2
+    assert [names[c] for c in res.centers] == ["0", "33"]
+    row = O.metric_row(g.offsets, g.nbr, g.wt, 10.0, res.cluster_index, res.num_clusters, lab, k, 1.0, 5.0)
+    assert row == ("0.3122945430637738,0.6486360381182862,0.6684671059738576,0.8319365867687499,"
+                   "0.9032258064516129,0.9117647058823529,0.8235294117647058,2,5")
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_karate_sweep_mutation(mode):
+    setup(N.KERNEL_FASTFWD, mode)
+    g, names, lab, k = H.karate()
+    grid = O.log_sigma_grid(10.0)
+    res, v, succ = N.cluster_sweep(g.csr(N), grid, want_v=True, want_succ=True)
+    counts = [r.num_clusters for r in res]
+    assert O.detect_mutation(grid, counts) == (2.272723014236749, 2.5555343651620004, 17)
+    for q, s in enumerate(grid):
+        vo, so, co, cio, ko = O.cluster(g.offsets, g.nbr, g.wt, 10.0, s, mode=mode)
+        assert_bits(v[q], vo)
+        assert np.array_equal(succ[q], so) and np.array_equal(res[q].center, co)
+        assert np.array_equal(res[q].cluster_index, cio) and res[q].num_clusters == ko
+
+
+@pytest.mark.parametrize("unit", [True, False])
+def test_cluster_sweep_random_graphs_labels(unit):
+    for n in (40, 301, 1000):
+        g = H.random_graph(n, 3.0, seed=45 + n, unit=unit)
+        sig = O.log_sigma_grid(10.0, 12)
+        res, v, succ = N.cluster_sweep(g.csr(N), sig, want_v=True, want_succ=True)
+        for q, s in enumerate(sig):
+            vo, so, co, cio, ko = O.cluster(g.offsets, g.nbr, g.wt, 10.0, s)
+            assert_bits(v[q], vo)
+            assert np.array_equal(succ[q], so)
+            assert np.array_equal(res[q].center, co) and np.array_equal(res[q].cluster_index, cio)
+            assert res[q].num_clusters == ko
+
+
+def test_build_successors_and_resolve_on_random_potentials():
+    # ggd_test.cpp:103-142 / acceptance criterion 4 (seed 45): random potentials
+    rng = np.random.default_rng(45)
+    for trial in range(20):
+        n = int(rng.integers(2, 300))
+        g = H.random_graph(n, 3.0, seed=trial)
+        v = rng.random(n)
+        if trial % 3 == 0:
+            v = np.round(v * 4) / 4  # exact ties -> smaller id
+        succ = N.build_successors(g.csr(N), v)
+        assert np.array_equal(succ, O.build_successors(g.offsets, g.nbr, v))
+        res = N.resolve_centers(succ)
+        co, cio, ko = O.resolve_centers(succ)
+        assert np.array_equal(res.center, co) and np.array_equal(res.cluster_index, cio) and res.num_clusters == ko
+
+
+def test_resolve_centers_errors_match_reference_order():
+    with pytest.raises(N.LogicError, match="successor map contains a cycle"):
+        N.resolve_centers(np.array([1, 0], np.int32))
+    with pytest.raises(ValueError, match="successor id out of range"):
+        N.resolve_centers(np.array([5, 0], np.int32))
+    # node 0 reaches a cycle before node 2 reaches an out-of-range id -> cycle
+    with pytest.raises(N.LogicError):
+        N.resolve_centers(np.array([1, 0, 7], np.int32))
+    # node 0 reaches the out-of-range id first
+    with pytest.raises(ValueError):
+        N.resolve_centers(np.array([2, 1, -1, 4, 3], np.int32))
+    res = N.resolve_centers(np.array([1, 2, 3, 3, 3], np.int32))
+    assert res.num_clusters == 1 and res.center.tolist() == [3] * 5
+    res = N.resolve_centers(np.array([0, 1, 2, 3], np.int32))
+    assert res.num_clusters == 4
+    with pytest.raises(ValueError, match="does not match graph size"):
+        N.build_successors(H.path(3).csr(N), np.array([1.0, 2.0]))
+
+
+def test_deep_chain_resolve():
+    # long successor chains (a path with monotone potentials) stay O(N log N)
+    n = 200_000
+    succ = np.maximum(np.arange(n, dtype=np.int32) - 1, 0)
+    res = N.resolve_centers(succ)
+    assert res.num_clusters == 1 and (res.center == 0).all()
+    g = H.path(5001)
+    v = np.arange(g.n, dtype=np.float64)
+    res = N.resolve_centers(N.build_successors(g.csr(N), v))
+    assert res.num_clusters == 1
+
+
+def test_tiny_sigma_star_fragments_and_collapses():
+    # sweep_test.cpp:72-89 (the underflow tie case)
+    g = H.star(8)
+    res = N.cluster(g.csr(N), 0.2)
+    assert res.num_clusters == 8 and all(res.center[l] == l for l in range(1, 9))
+    res = N.cluster(g.csr(N), 0.01)
+    assert res.num_clusters == 1 and res.centers.tolist() == [0]
+
+
+def test_device_api_row_shards_assemble_to_full_field():
+    import torch
+    g = H.random_graph(5003, 8.0, seed=3, unit=True)
+    dg = N.DeviceCsr(g.csr(N))
+    sig = O.log_sigma_grid(10.0, 32)
+    full = torch.empty((g.n, len(sig)), dtype=torch.float64, device="cuda")
+    N.dev_potentials(dg, sig, 0, g.n, full)
+    parts = []
+    bounds = [0, 1000, 1001, 3333, 5003]
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        t = torch.empty((b - a, len(sig)), dtype=torch.float64, device="cuda")
+        N.dev_potentials(dg, sig, a, b, t)
+        parts.append(t)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(parts).view(torch.int64), full.view(torch.int64))
+    host = N.potentials(g.csr(N), sig)
+    assert_bits(full.cpu().numpy().T.copy(), host)
+    S = len(sig)
+    succ = torch.empty((S, g.n), dtype=torch.int32, device="cuda")
+    center = torch.empty_like(succ)
+    ci = torch.empty_like(succ)
+    nc = torch.empty(S, dtype=torch.int32, device="cuda")
+    ws = torch.empty(N.dev_ggd_workspace(g.n, S), dtype=torch.uint8, device="cuda")
+    N.dev_ggd(dg, full, S, succ, center, ci, nc, ws)
+    torch.cuda.synchronize()
+    res, _, s_host = N.cluster_sweep(g.csr(N), sig, want_succ=True)
+    assert np.array_equal(succ.cpu().numpy(), s_host)
+    assert np.array_equal(center.cpu().numpy(), np.stack([r.center for r in res]))
+    assert nc.cpu().tolist() == [r.num_clusters for r in res]
