@@ -84,6 +84,7 @@ struct DevBuf {
 
 struct DeviceCtx {
     cudaStream_t stream = nullptr;
+    cudaMemPool_t pool = nullptr;  // stream-ordered scratch that keeps its memory
     DevBuf off, nbr, w, v_nm, v_sm, succ, center, ci, nc, ws, tail, entry;
 };
 
@@ -98,6 +99,15 @@ DeviceCtx& ctx() {
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     DeviceCtx& c = all[dev];
     if (!c.stream) cuda_check(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    if (!c.pool) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cuda_check(cudaMemPoolCreate(&c.pool, &props), "cudaMemPoolCreate");
+        std::uint64_t keep = ~0ull;
+        cuda_check(cudaMemPoolSetAttribute(c.pool, cudaMemPoolAttrReleaseThreshold, &keep), "cudaMemPoolSetAttribute");
+    }
     return c;
 }
 
@@ -231,7 +241,7 @@ void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S,
             P.entry_ld = Sc;
             P.entry_col0 = 0;
         }
-        cuda_check(launch_potentials(P, g_opt.kernel, st), "potential kernel launch");
+        cuda_check(launch_potentials(P, g_opt.kernel, C.pool, st), "potential kernel launch");
     }
 }
 
@@ -379,7 +389,7 @@ gqc_status gqc_resolve_centers(int32_t n, const int32_t* succ, int32_t* center, 
         cuda_check(cudaMemcpyAsync(ds, succ, n * sizeof(int), cudaMemcpyHostToDevice, st), "copy succ");
         int err = 0;
         int k = 0;
-        cuda_check(resolve_checked(n, ds, dc, dci, &k, &err, st), "resolve centers");
+        cuda_check(resolve_checked(n, ds, dc, dci, &k, &err, C.pool, st), "resolve centers");
         if (err == 1) fail(GQC_EINVAL, "successor id out of range");  // ggd.cpp:37-38
         if (err == 2) fail(GQC_ECYCLE, "successor map contains a cycle");  // ggd.cpp:41
         cuda_check(cudaMemcpyAsync(center, dc, n * sizeof(int), cudaMemcpyDeviceToHost, st), "copy center");

@@ -1,0 +1,282 @@
+// Exact fast-forward of sequential fp64 adds (the heart of the FASTFWD
+// potential kernel). Host/device portable so the algorithm is unit-tested on
+// the CPU against naive sequential adds (tests/test_ff_cpu.py) with the same
+// source the sm_100a kernel compiles. Host builds must use -ffp-contract=off.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#if defined(__CUDACC__)
+#define GQC_HD __host__ __device__
+#else
+#define GQC_HD
+#endif
+
+namespace gqc {
+namespace ffc {
+
+#if defined(__CUDA_ARCH__)
+__device__ __forceinline__ double gqc_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double gqc_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double gqc_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double gqc_div(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double gqc_fma(double a, double b, double c) { return __fma_rn(a, b, c); }
+// ~1/a for normal a: MUFU approximation + one Newton step (relative error
+// ~2^-44; the jump count it feeds is corrected exactly, see max_steps).
+__device__ __forceinline__ double gqc_rcp(double a) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+    const double e = __fma_rn(-a, r, 1.0);
+    return __fma_rn(r, e, r);
+}
+__device__ __forceinline__ double gqc_floor(double a) { return floor(a); }
+__device__ __forceinline__ long long gqc_bits(double a) { return __double_as_longlong(a); }
+__device__ __forceinline__ int gqc_ffsll(long long a) { return __ffsll(a); }
+__device__ __forceinline__ int gqc_max(int a, int b) { return max(a, b); }
+__device__ __forceinline__ bool gqc_lo_odd(double a) { return __double2loint(a) & 1; }
+__device__ __forceinline__ int exp_field(double x) { return (__double2hiint(x) >> 20) & 0x7ff; }
+// 2^(f - 1023) for a biased exponent f in [1, 2046]
+__device__ __forceinline__ double pow2_field(int f) { return __hiloint2double(f << 20, 0); }
+#else
+inline double gqc_add(double a, double b) { return a + b; }
+inline double gqc_sub(double a, double b) { return a - b; }
+inline double gqc_mul(double a, double b) { return a * b; }
+inline double gqc_div(double a, double b) { return a / b; }
+inline double gqc_fma(double a, double b, double c) { return std::fma(a, b, c); }
+inline double gqc_rcp(double a) { return 1.0 / a; }
+inline double gqc_floor(double a) { return std::floor(a); }
+inline long long gqc_bits(double a) {
+    long long b;
+    std::memcpy(&b, &a, sizeof b);
+    return b;
+}
+inline int gqc_ffsll(long long a) { return __builtin_ffsll(a); }
+inline int gqc_max(int a, int b) { return a > b ? a : b; }
+inline bool gqc_lo_odd(double a) { return gqc_bits(a) & 1; }
+inline int exp_field(double x) { return static_cast<int>((gqc_bits(x) >> 52) & 0x7ff); }
+inline double pow2_field(int f) {
+    const long long b = static_cast<long long>(f) << 52;
+    double d;
+    std::memcpy(&d, &b, sizeof d);
+    return d;
+}
+#endif
+
+// ---------------------------------------------------------------------------
+// Exact fast-forward of L sequential adds s <- fl(s + c), s >= 0, c >= 0.
+//
+// Inside a binade [base, 2 base) of s (unit in the last place u = base*2^-52;
+// the subnormals share u = 2^-1074 with [2^-1022, 2^-1021) and are treated as
+// that binade), an add whose exact result stays <= 2 base rounds on the
+// u-grid, so fl(s + c) = s + inc with inc = round_u(c). round_u(c) can depend
+// on the parity of s/u only when c is an exact half-ulp tie (for a given c
+// that happens in exactly one binade, f_tie), and a tie always lands on an
+// even multiple, after which the increment is constant. inc is read off an
+// even reference point, inc = fl(base + c) - base; an odd s in the tie binade
+// takes one real step first. A run that ends inside the binade is one exact
+// fma (s + L*inc lies on the u-grid below 2 base). A run that reaches the top
+// jumps the m = floor((2 base - u - s) / inc) steps that provably stay inside
+// (their exact sums stay below 2 base - u/2), then crosses with one real add.
+// c >= base/2 (at most two adds per binade) is stepped with real adds, and
+// inc == 0 (c <= u/2) is a fixed point after at most one real add.
+//
+// A Chain caches the binade parameters of its partial sum, so runs that stay
+// inside a binade (the common case once the sum is large) cost one fma and
+// the per-binade work is paid once per crossing. The state is kept minimal
+// (three doubles and two ints) because the kernel holds two chains per thread
+// and its occupancy is register-bound.
+// ---------------------------------------------------------------------------
+struct Chain {
+    double s;    // partial sum
+    double top;  // 2 base of the cached binade (0: no cache)
+    double inc;  // settled increment in the cached binade
+    int f_tie;   // binade in which c is a half-ulp tie
+    int flags;   // bit 0: c < base/2 (jumpable); bit 1: cached binade == f_tie
+};
+constexpr int kJump = 1;
+constexpr int kTie = 2;
+
+// Biased exponent f of the binade whose half-ulp is the lowest set bit of c.
+GQC_HD inline int tie_binade(const double c) {
+    const long long bits = gqc_bits(c);
+    int e = static_cast<int>((bits >> 52) & 0x7ff);
+    long long mant = bits & ((1ll << 52) - 1);
+    if (e > 0) mant |= (1ll << 52);
+    else e = 1;
+    return e + gqc_ffsll(mant);  // e + 1 + (index of the lowest set bit)
+}
+
+GQC_HD inline Chain make_chain(const double s, const double c) {
+    Chain ch;
+    ch.s = s;
+    ch.top = 0.0;
+    ch.inc = 0.0;
+    ch.f_tie = tie_binade(c);
+    ch.flags = 0;
+    return ch;
+}
+
+GQC_HD inline void refresh(Chain& ch, const double c) {
+    const int f = gqc_max(exp_field(ch.s), 1);
+    const double base = pow2_field(f);
+    ch.top = gqc_add(base, base);
+    const bool jump = c < gqc_mul(base, 0.5);
+    ch.inc = jump ? gqc_sub(gqc_add(base, c), base) : 0.0;
+    ch.flags = (jump ? kJump : 0) | (f == ch.f_tie ? kTie : 0);
+}
+
+// In-binade fast path is allowed: jumpable and not (tie binade with odd s).
+GQC_HD inline bool settled(const Chain& ch) {
+    return (ch.flags & kJump) && !((ch.flags & kTie) && gqc_lo_odd(ch.s));
+}
+
+// Exact jump count of the slow path: the largest m with s + m*inc <= top - u.
+// The true quotient is < L <= 2^31 wherever this is called, so the estimate is
+// off by at most one and the two fma sign tests (exact: room - m*inc is a
+// u-grid multiple) settle it. Tiny binades (1/inc would overflow) divide.
+GQC_HD inline double max_steps(const Chain& ch, const double room) {
+    const double q = ch.top > 0x1p-950 ? gqc_mul(room, gqc_rcp(ch.inc)) : gqc_div(room, ch.inc);
+    double m = gqc_floor(q);
+    if (gqc_fma(-m, ch.inc, room) < 0.0) m = m - 1.0;
+    else if (gqc_fma(-(m + 1.0), ch.inc, room) >= 0.0) m = m + 1.0;
+    return m;
+}
+
+GQC_HD inline double room_of(const Chain& ch) {
+    const double u = gqc_mul(ch.top, 0x1p-53);
+    return gqc_sub(gqc_sub(ch.top, u), ch.s);
+}
+
+// L sequential adds of c (the general loop).
+GQC_HD inline void ff_run(Chain& ch, const double c, int L) {
+    while (L > 0) {
+        if (!(ch.s < ch.top)) refresh(ch, c);
+        if (!(ch.flags & kJump)) {  // c >= base/2: real adds
+            ch.s = gqc_add(ch.s, c);
+            --L;
+            continue;
+        }
+        if (ch.inc == 0.0) {  // c <= u/2: fixed point after one add
+            ch.s = gqc_add(ch.s, c);
+            return;
+        }
+        if ((ch.flags & kTie) && gqc_lo_odd(ch.s)) {  // settle tie parity
+            ch.s = gqc_add(ch.s, c);
+            --L;
+            continue;
+        }
+        const double t = gqc_fma(static_cast<double>(L), ch.inc, ch.s);
+        if (t < ch.top) {  // the whole remainder stays in the binade: exact
+            ch.s = t;
+            return;
+        }
+        const double m = max_steps(ch, room_of(ch));
+        ch.s = gqc_fma(m, ch.inc, ch.s);  // exact: a u-grid point below 2 base
+        L -= static_cast<int>(m);
+        ch.s = gqc_add(ch.s, c);  // crosses into the next binade
+        --L;
+    }
+}
+
+// One step of the convergent two-chain loop for a chain with Lx adds left:
+// the whole remainder if it stays in the binade (one exact fma; inc == 0 is
+// the fixed point t == s), else the maximal in-binade jump plus the crossing
+// add, else (c >= base/2, or a half-ulp tie at odd s) one real add. Written
+// as selects so the lanes of a warp stay converged whatever case each lane
+// is in.
+GQC_HD inline void ff_step(Chain& ch, const double c, int& Lx) {
+    if (!(ch.s < ch.top)) refresh(ch, c);
+    const bool ok = settled(ch);
+    const double t = gqc_fma(static_cast<double>(Lx), ch.inc, ch.s);
+    if (ok && t < ch.top) {
+        ch.s = t;
+        Lx = 0;
+        return;
+    }
+    double m = 0.0;
+    if (ok) m = max_steps(ch, room_of(ch));
+    ch.s = gqc_add(gqc_fma(m, ch.inc, ch.s), c);
+    Lx -= static_cast<int>(m) + 1;
+}
+
+// Both chains of a W run of length L, advanced together until both are done.
+GQC_HD inline void ff_run2(Chain& a, const double ca, Chain& b, const double cb, const int L) {
+    int La = L, Lb = L;
+    do {
+        if (La > 0) ff_step(a, ca, La);
+        if (Lb > 0) ff_step(b, cb, Lb);
+    } while (La > 0 || Lb > 0);
+}
+
+// ---------------------------------------------------------------------------
+// Prefix segments of the pure trajectory P(t) = t sequential adds of c from
+// s = 0 (every row's first run, before its first neighbour or itself, is such
+// a run). Segment k covers [t[k], t[k+1]) with P(t) = s0[k] + (t - t[k])*inc[k]
+// exactly (inc 0 for single real steps and for the final fixed point). The
+// builder follows ff_run step for step; from t_end on the caller continues
+// from s_end with ff_run.
+// ---------------------------------------------------------------------------
+constexpr int kPrefixCap = 96;
+constexpr int kPrefixForever = 0x7fffffff;
+
+GQC_HD inline void build_prefix(const double c, const int n, int* t_out, double* s_out, double* inc_out,
+                                int* count, int* t_end, double* s_end) {
+    Chain ch = make_chain(0.0, c);
+    int t = 0, k = 0;
+    while (t < n && k < kPrefixCap - 1) {
+        if (!(ch.s < ch.top)) refresh(ch, c);
+        if (!(ch.flags & kJump) || (ch.inc != 0.0 && !settled(ch))) {  // single real step
+            t_out[k] = t;
+            s_out[k] = ch.s;
+            inc_out[k] = 0.0;
+            ++k;
+            ch.s = gqc_add(ch.s, c);
+            ++t;
+            continue;
+        }
+        if (ch.inc == 0.0) {  // one add, then a fixed point forever
+            t_out[k] = t;
+            s_out[k] = ch.s;
+            inc_out[k] = 0.0;
+            ++k;
+            ch.s = gqc_add(ch.s, c);
+            ++t;
+            t_out[k] = t;
+            s_out[k] = ch.s;
+            inc_out[k] = 0.0;
+            ++k;
+            t = kPrefixForever;
+            break;
+        }
+        double m = max_steps(ch, room_of(ch));
+        if (m > static_cast<double>(n - t)) m = static_cast<double>(n - t);
+        t_out[k] = t;  // valid for [t, t + m]
+        s_out[k] = ch.s;
+        inc_out[k] = ch.inc;
+        ++k;
+        ch.s = gqc_fma(m, ch.inc, ch.s);
+        t += static_cast<int>(m);
+        if (t >= n) break;
+        ch.s = gqc_add(ch.s, c);  // crossing
+        ++t;
+    }
+    *count = k;
+    *t_end = t;
+    *s_end = ch.s;
+}
+
+// P(L) for 0 <= L < t_end, by binary search for the last segment start <= L.
+GQC_HD inline double prefix_value(const int* t, const double* s0, const double* inc, const int count, const int L) {
+    int lo = 0, hi = count - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (t[mid] <= L) lo = mid;
+        else hi = mid - 1;
+    }
+    return gqc_fma(static_cast<double>(L - t[lo]), inc[lo], s0[lo]);
+}
+
+}  // namespace ffc
+}  // namespace gqc

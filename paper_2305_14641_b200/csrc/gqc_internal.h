@@ -50,7 +50,9 @@ struct PotentialLaunch {
 };
 
 // Kernel launchers (kernels.cu). Return a cudaError_t as int.
-int launch_potentials(const PotentialLaunch& p, int kernel, void* stream);
+// Stream-ordered scratch comes from `pool` (a cudaMemPool_t that keeps its
+// memory, so per-call scratch costs no driver allocation).
+int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* stream);
 int launch_successors(std::int32_t n, const std::int64_t* offsets, const std::int32_t* nbr, const double* v,
                       std::int32_t n_sigma, std::int32_t* succ_sm, void* stream);
 int launch_chase(std::int32_t n, std::int32_t n_sigma, const std::int32_t* succ_sm, std::int32_t* center_sm,
@@ -62,7 +64,8 @@ int launch_transpose(const double* v_nm, std::int32_t n, std::int32_t n_sigma, d
 // Checked resolve for arbitrary successor maps: writes center/cluster_index,
 // returns status via *err_kind (0 ok, 1 out of range, 2 cycle) on the host.
 int resolve_checked(std::int32_t n, const std::int32_t* succ_dev, std::int32_t* center_dev,
-                    std::int32_t* cluster_index_dev, std::int32_t* num_clusters_host, int* err_kind, void* stream);
+                    std::int32_t* cluster_index_dev, std::int32_t* num_clusters_host, int* err_kind, void* pool,
+                    void* stream);
 
 // Launch accounting (kernels issued by the last C-ABI call).
 void count_launch(int k = 1);

@@ -24,61 +24,10 @@ namespace {
 
 constexpr int kBlock = 256;
 
-__device__ __forceinline__ int exp_field(double x) { return (__double2hiint(x) >> 20) & 0x7ff; }
-// 2^(f - 1023) for a biased exponent f in [1, 2046]
-__device__ __forceinline__ double pow2_field(int f) { return __hiloint2double(f << 20, 0); }
 
-// ---------------------------------------------------------------------------
-// Exact fast-forward of L sequential adds s <- fl(s + c), s >= 0, c >= 0.
-//
-// Inside a binade [base, 2 base) of s (unit in the last place u = base*2^-52;
-// the subnormals share u = 2^-1074 with [2^-1022, 2^-1021) and are treated as
-// that binade), an add whose exact result stays <= 2 base rounds on the
-// u-grid, so fl(s + c) = s + inc with inc = round_u(c). round_u(c) can depend
-// on the parity of s/u only when c is an exact half-ulp tie, and a tie always
-// lands on an even multiple, after which the increment is constant. inc is
-// read off an even reference point, inc = fl(base + c) - base; odd s with a
-// tie takes one real step first. Then m = floor((2 base - u - s) / inc) steps
-// are all exact grid steps (their exact sums stay below 2 base - u/2) and are
-// taken at once; the binade crossing itself is always a real add. c >= base/2
-// (at most two adds per binade) and inc == 0 (a fixed point after at most one
-// real add) are handled by real adds. Work: O(number of binades crossed).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ double ff_chain(double s, const double c, int L) {
-    if (c == 0.0) return s;
-    while (L > 0) {
-        const int f = max(exp_field(s), 1);
-        const double base = pow2_field(f);
-        if (!(c < __dmul_rn(base, 0.5))) {
-            s = __dadd_rn(s, c);
-            --L;
-            continue;
-        }
-        const double inc = __dsub_rn(__dadd_rn(base, c), base);
-        if (inc == 0.0) return __dadd_rn(s, c);
-        const double u = __dmul_rn(base, 0x1p-52);
-        if (__double2loint(s) & 1) {
-            const double bo = __dadd_rn(base, u);
-            if (__dsub_rn(__dadd_rn(bo, c), bo) != inc) {  // half-ulp tie: settle parity
-                s = __dadd_rn(s, c);
-                --L;
-                continue;
-            }
-        }
-        const double room = __dsub_rn(__dsub_rn(__dadd_rn(base, base), s), u);
-        if (room < inc) {  // crossing into the next binade
-            s = __dadd_rn(s, c);
-            --L;
-            continue;
-        }
-        double m = floor(__ddiv_rn(room, inc));
-        m = fmin(m, static_cast<double>(L));
-        if (__fma_rn(-m, inc, room) < 0.0) m = m - 1.0;  // exact sign of room - m*inc
-        s = __dadd_rn(s, __dmul_rn(m, inc));               // exact: a u-grid point below 2 base
-        L -= static_cast<int>(m);
-    }
-    return s;
-}
+#include "ff_chain.cuh"
+
+using namespace gqc::ffc;
 
 // K1: the dense in-order replay, two independent chains per thread.
 __device__ __forceinline__ void replay(double& num, double& den, const double p, const double e, int L) {
@@ -92,14 +41,21 @@ __device__ __forceinline__ void replay(double& num, double& den, const double p,
     den = b;
 }
 
+// A run of L identical (p, e) neighbour terms (consecutive columns with the
+// same weight). Rare outside dense rows; kept out of line (by value, so the
+// caller's chains stay in registers).
 template <bool kFF>
-__device__ __forceinline__ void run(double& num, double& den, const double p, const double e, const int L) {
-    if (L <= 0) return;
+__device__ __noinline__ double2 term_run_long(const double ns, const double ds, const double p, const double e,
+                                              const int L) {
     if constexpr (kFF) {
-        num = ff_chain(num, p, L);
-        den = ff_chain(den, e, L);
+        Chain a = make_chain(ns, p), b = make_chain(ds, e);
+        ff_run(a, p, L);
+        ff_run(b, e, L);
+        return make_double2(a.s, b.s);
     } else {
-        replay(num, den, p, e, L);
+        double a = ns, b = ds;
+        replay(a, b, p, e, L);
+        return make_double2(a, b);
     }
 }
 
@@ -129,12 +85,52 @@ __device__ __noinline__ double pexp_dev(const double x0) {
 }
 
 // ---------------------------------------------------------------------------
+// Prefix builder: one thread per (sigma, chain) records the pure trajectory of
+// the non-adjacent constant from 0 (ff_chain.cuh, build_prefix). Layout per
+// (sigma, chain) q = 2*s + {0 num, 1 den}: kPrefixCap entries of t / s0 / inc.
+// ---------------------------------------------------------------------------
+struct PrefixTable {
+    int* t;
+    double* s0;
+    double* inc;
+    int* count;
+    int* t_end;
+    double* s_end;
+};
+
+__global__ void prefix_kernel(const __grid_constant__ PotentialLaunch P, PrefixTable T) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= 2 * P.n_sigma) return;
+    const SigmaConsts& c = P.c[q >> 1];
+    const double cst = (q & 1) ? c.eW : c.pW;
+    build_prefix(cst, P.n, T.t + q * kPrefixCap, T.s0 + q * kPrefixCap, T.inc + q * kPrefixCap, T.count + q,
+                 T.t_end + q, T.s_end + q);
+}
+
+// Value of the first run (L pure adds from 0) for chain q, then the chain's
+// binade cache is invalidated so the next run refreshes it.
+__device__ __forceinline__ void first_run(Chain& ch, const double c, const PrefixTable& T, const int q, const int L) {
+    const int t_end = T.t_end[q];
+    if (L < t_end) {
+        ch.s = prefix_value(T.t + q * kPrefixCap, T.s0 + q * kPrefixCap, T.inc + q * kPrefixCap, T.count[q], L);
+    } else {
+        ch.s = T.s_end[q];
+        ff_run(ch, c, L - t_end);
+    }
+    ch.top = 0.0;
+}
+
+// ---------------------------------------------------------------------------
 // Potential kernel: thread = (row, sigma), sigma fastest, so the lanes of a
 // warp share one CSR row (broadcast loads) and write one contiguous node-major
 // slice of V. Grid: ceil(rows * n_sigma / 256) blocks of 256 threads.
+// Row walk: runs of non-adjacent columns between the ascending breakpoints
+// (neighbours and the row itself); K2 takes the first run from the prefix
+// table and every later run through the two-chain fast-forward.
 // ---------------------------------------------------------------------------
 template <bool kFF, int kW>
-__global__ void __launch_bounds__(kBlock) potential_kernel(const __grid_constant__ PotentialLaunch P) {
+__global__ void __launch_bounds__(kBlock) potential_kernel(const __grid_constant__ PotentialLaunch P,
+                                                           const PrefixTable T) {
     __shared__ double sc[kSigmaFields][kMaxSigmaPerLaunch];
     for (int idx = threadIdx.x; idx < kSigmaFields * kMaxSigmaPerLaunch; idx += blockDim.x) {
         const int ss = idx % kMaxSigmaPerLaunch, f = idx / kMaxSigmaPerLaunch;
@@ -149,17 +145,13 @@ __global__ void __launch_bounds__(kBlock) potential_kernel(const __grid_constant
     if (r64 >= P.row_end) return;
     const int i = static_cast<int>(r64);
 
-    const double inv = sc[0][s], neg_inv = sc[1][s];
-    const double eW = sc[2][s], pW = sc[3][s];
     const double e1 = sc[4][s], p1 = sc[5][s];
-    const double eWt = sc[6][s], pWt = sc[7][s];
-    const double e1t = sc[8][s], p1t = sc[9][s];
-
     const int n = P.n;
     const bool tail = P.tail != 0;
     const long long kend = P.offsets[i + 1];
     long long k = P.offsets[i];
-    double num = 0.0, den = 0.0;
+    const double pW = sc[3][s], eW = sc[2][s];
+    Chain num = make_chain(0.0, pW), den = make_chain(0.0, eW);
     int pos = 0;
     bool self_pending = true;
 
@@ -176,20 +168,30 @@ __global__ void __launch_bounds__(kBlock) potential_kernel(const __grid_constant
             col = n;
             kind = 0;
         }
-        // non-adjacent run over [pos, col)
+        // non-adjacent run over [pos, col); the first run never reaches the
+        // tail column (it stops at or before the row's own column)
         const int L = col - pos;
         if (L > 0) {
-            if (tail && col == n) {
-                run<kFF>(num, den, pW, eW, L - 1);
-                num = __dadd_rn(num, pWt);
-                den = __dadd_rn(den, eWt);
+            const bool at_end = tail && col == n;
+            const int Lw = at_end ? L - 1 : L;
+            if constexpr (kFF) {
+                if (pos == 0) {
+                    first_run(num, pW, T, 2 * s, Lw);
+                    first_run(den, eW, T, 2 * s + 1, Lw);
+                } else if (Lw > 0) {
+                    ff_run2(num, pW, den, eW, Lw);
+                }
             } else {
-                run<kFF>(num, den, pW, eW, L);
+                replay(num.s, den.s, pW, eW, Lw);
+            }
+            if (at_end) {
+                num.s = __dadd_rn(num.s, sc[7][s]);
+                den.s = __dadd_rn(den.s, sc[6][s]);
             }
         }
         if (kind == 0) break;
         if (kind == 1) {  // self: d2 = 0, exp(-0) = 1 -> num += 0, den += 1
-            den = __dadd_rn(den, 1.0);
+            den.s = __dadd_rn(den.s, 1.0);
             self_pending = false;
             pos = col + 1;
             continue;
@@ -213,8 +215,8 @@ __global__ void __launch_bounds__(kBlock) potential_kernel(const __grid_constant
         }
         double e, p;
         if constexpr (kW == kUnit) {
-            e = at_tail ? e1t : e1;
-            p = at_tail ? p1t : p1;
+            e = at_tail ? sc[8][s] : e1;
+            p = at_tail ? sc[9][s] : p1;
         } else {
             const double d2 = __dmul_rn(wk, wk);
             if constexpr (kW == kEntryTable) {
@@ -230,16 +232,25 @@ __global__ void __launch_bounds__(kBlock) potential_kernel(const __grid_constant
                     }
                     e = __ldg(P.tail_exp + (lo - b0) * S + s);
                 } else {
-                    e = pexp_dev(__dmul_rn(neg_inv, d2));
+                    e = pexp_dev(__dmul_rn(sc[1][s], d2));
                 }
             }
             p = __dmul_rn(d2, e);
         }
-        run<kFF>(num, den, p, e, end - col);
+        const int cnt = end - col;
+        if (cnt == 1) {
+            num.s = __dadd_rn(num.s, p);
+            den.s = __dadd_rn(den.s, e);
+        } else {
+            const double2 r = term_run_long<kFF>(num.s, den.s, p, e, cnt);
+            num.s = r.x;
+            den.s = r.y;
+        }
         k = kk;
         pos = end;
     }
-    P.out[static_cast<long long>(i - P.row_begin) * P.out_ld + P.out_col0 + s] = __dmul_rn(inv, __ddiv_rn(num, den));
+    P.out[static_cast<long long>(i - P.row_begin) * P.out_ld + P.out_col0 + s] =
+        __dmul_rn(sc[0][s], __ddiv_rn(num.s, den.s));
 }
 
 // ---------------------------------------------------------------------------
@@ -372,28 +383,49 @@ int grid_for(long long threads) { return static_cast<int>((threads + kBlock - 1)
 
 }  // namespace
 
-int launch_potentials(const PotentialLaunch& p, int kernel, void* stream) {
+int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* stream) {
     const long long threads = static_cast<long long>(p.row_end - p.row_begin) * p.n_sigma;
     if (threads <= 0) return cudaSuccess;
     auto st = static_cast<cudaStream_t>(stream);
     const dim3 grid(grid_for(threads));
     const bool ff = kernel == 0;
+    PrefixTable T{};
+    void* mem = nullptr;
+    if (ff) {
+        // stream-ordered scratch: safe for concurrent calls on other streams
+        const int q = 2 * p.n_sigma;
+        const std::size_t bytes = static_cast<std::size_t>(q) * kPrefixCap * (sizeof(int) + 2 * sizeof(double)) +
+                                  static_cast<std::size_t>(q) * (2 * sizeof(int) + sizeof(double)) + 64;
+        cudaError_t e = cudaMallocFromPoolAsync(&mem, bytes, static_cast<cudaMemPool_t>(pool), st);
+        if (e != cudaSuccess) return e;
+        char* b = static_cast<char*>(mem);
+        T.s0 = reinterpret_cast<double*>(b);
+        T.inc = T.s0 + q * kPrefixCap;
+        T.s_end = T.inc + q * kPrefixCap;
+        T.t = reinterpret_cast<int*>(T.s_end + q);
+        T.count = T.t + q * kPrefixCap;
+        T.t_end = T.count + q;
+        prefix_kernel<<<1, 64, 0, st>>>(p, T);
+        count_launch();
+    }
     switch (p.weight_mode) {
         case kUnit:
-            if (ff) potential_kernel<true, kUnit><<<grid, kBlock, 0, st>>>(p);
-            else potential_kernel<false, kUnit><<<grid, kBlock, 0, st>>>(p);
+            if (ff) potential_kernel<true, kUnit><<<grid, kBlock, 0, st>>>(p, T);
+            else potential_kernel<false, kUnit><<<grid, kBlock, 0, st>>>(p, T);
             break;
         case kDevicePexp:
-            if (ff) potential_kernel<true, kDevicePexp><<<grid, kBlock, 0, st>>>(p);
-            else potential_kernel<false, kDevicePexp><<<grid, kBlock, 0, st>>>(p);
+            if (ff) potential_kernel<true, kDevicePexp><<<grid, kBlock, 0, st>>>(p, T);
+            else potential_kernel<false, kDevicePexp><<<grid, kBlock, 0, st>>>(p, T);
             break;
         default:
-            if (ff) potential_kernel<true, kEntryTable><<<grid, kBlock, 0, st>>>(p);
-            else potential_kernel<false, kEntryTable><<<grid, kBlock, 0, st>>>(p);
+            if (ff) potential_kernel<true, kEntryTable><<<grid, kBlock, 0, st>>>(p, T);
+            else potential_kernel<false, kEntryTable><<<grid, kBlock, 0, st>>>(p, T);
             break;
     }
     count_launch();
-    return cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
+    if (mem) cudaFreeAsync(mem, st);
+    return e;
 }
 
 int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nbr, const double* v, int n_sigma,
@@ -454,18 +486,19 @@ int launch_transpose(const double* v_nm, int n, int n_sigma, double* v_sm, void*
 }
 
 int resolve_checked(int n, const std::int32_t* succ_dev, std::int32_t* center_dev, std::int32_t* ci_dev,
-                    std::int32_t* num_clusters_host, int* err_kind, void* stream) {
+                    std::int32_t* num_clusters_host, int* err_kind, void* pool_, void* stream) {
+    auto pool = static_cast<cudaMemPool_t>(pool_);
     auto st = static_cast<cudaStream_t>(stream);
     int *p0, *t0, *p1, *t1, *nc;
     unsigned long long* first;
     const std::size_t bytes = sizeof(int) * static_cast<std::size_t>(n);
-    cudaError_t e = cudaMallocAsync(&p0, bytes * 4 + 64, st);
+    cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p0), bytes * 4 + 64, pool, st);
     if (e != cudaSuccess) return e;
     int* const alloc = p0;
     t0 = p0 + n;
     p1 = t0 + n;
     t1 = p1 + n;
-    first = reinterpret_cast<unsigned long long*>(t1 + n + (n & 1));
+    first = reinterpret_cast<unsigned long long*>(p0 + 4 * static_cast<std::size_t>(n));  // 16n bytes: 8-aligned
     nc = reinterpret_cast<int*>(first + 1);
     const int g = grid_for(n);
     resolve_init_kernel<<<g, kBlock, 0, st>>>(n, succ_dev, p0, t0);
@@ -494,7 +527,7 @@ int resolve_checked(int n, const std::int32_t* succ_dev, std::int32_t* center_de
         cudaMemcpyAsync(center_dev, p0, bytes, cudaMemcpyDeviceToDevice, st);
         std::size_t ws = labels_workspace_bytes(n, 1);
         void* wsp = nullptr;
-        e = cudaMallocAsync(&wsp, ws, st);
+        e = cudaMallocFromPoolAsync(&wsp, ws, pool, st);
         if (e == cudaSuccess) {
             e = static_cast<cudaError_t>(launch_labels(n, 1, center_dev, ci_dev, nc, wsp, ws, st));
             cudaMemcpyAsync(num_clusters_host, nc, sizeof(int), cudaMemcpyDeviceToHost, st);

@@ -1,0 +1,247 @@
+// CPU harness for the exact fast-forward (paper_2305_14641_b200/csrc/ff_chain.cuh):
+// the same source the sm_100a kernel compiles, checked against naive
+// sequential adds on randomized cases (binade crossings, half-ulp ties,
+// subnormals, fixed points) and on row-like sequences of runs and terms.
+// Built by tests/test_ff_cpu.py with g++ -O2 -ffp-contract=off (no -march).
+#include <cstdint>
+#include <cstring>
+
+#include "ff_chain.cuh"
+
+using namespace gqc::ffc;
+
+namespace {
+
+struct Rng {
+    std::uint64_t s;
+    std::uint64_t next() {
+        std::uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    }
+    double uni() { return (next() >> 11) * 0x1.0p-53; }
+    int below(int n) { return static_cast<int>(uni() * n); }
+};
+
+double from_bits(std::uint64_t b) {
+    double d;
+    std::memcpy(&d, &b, sizeof d);
+    return d;
+}
+
+// A positive double with a random biased exponent in [elo, ehi] (0 = subnormal)
+// and a mantissa with a random number of trailing zero bits (ties).
+double rand_double(Rng& r, int elo, int ehi) {
+    const int e = elo + r.below(ehi - elo + 1);
+    std::uint64_t mant = r.next() & ((1ull << 52) - 1);
+    const int tz = r.below(4) == 0 ? r.below(53) : 0;
+    if (tz > 0) mant &= ~((1ull << tz) - 1);
+    if (e == 0 && mant == 0) mant = 1;
+    return from_bits((static_cast<std::uint64_t>(e) << 52) | mant);
+}
+
+double naive(double s, double c, long long L) {
+    for (long long t = 0; t < L; ++t) s = s + c;
+    return s;
+}
+
+int rand_len(Rng& r, int maxL) {
+    // log-uniform in [1, maxL]
+    const double x = r.uni() * __builtin_log(static_cast<double>(maxL));
+    int L = static_cast<int>(__builtin_exp(x));
+    return L < 1 ? 1 : (L > maxL ? maxL : L);
+}
+
+}  // namespace
+
+extern "C" {
+
+// Single runs from arbitrary (s, c, L). Returns the number of mismatches;
+// the first one is written to bad[0..2] = (s, c, L).
+long long fft_single(std::uint64_t seed, int ncases, int maxL, double* bad) {
+    Rng r{seed};
+    long long mism = 0;
+    for (int k = 0; k < ncases; ++k) {
+        const int mode = r.below(5);
+        double c, s;
+        if (mode == 0) {  // subnormal / tiny regime
+            c = rand_double(r, 0, 3);
+            s = r.below(3) == 0 ? 0.0 : rand_double(r, 0, 6);
+        } else {
+            const int ec = 1 + r.below(1100);
+            c = rand_double(r, ec > 2000 ? 2000 : ec, ec > 2000 ? 2000 : ec);
+            const int es = ec + r.below(70) - 8;
+            s = (mode == 1 || es < 0) ? 0.0 : rand_double(r, es < 0 ? 0 : es, es < 0 ? 0 : (es > 2000 ? 2000 : es));
+        }
+        const int L = rand_len(r, maxL);
+        Chain ch = make_chain(s, c);
+        ff_run(ch, c, L);
+        const double ref = naive(s, c, L);
+        if (std::memcmp(&ch.s, &ref, sizeof ref) != 0) {
+            if (mism == 0 && bad) {
+                bad[0] = s;
+                bad[1] = c;
+                bad[2] = L;
+            }
+            ++mism;
+        }
+    }
+    return mism;
+}
+
+// Row-like sequences: a chain with a fixed W constant receives runs of W
+// terms interleaved with single larger terms (neighbours) and a +1 (self),
+// the cache persisting across runs exactly as in the kernel.
+long long fft_rows(std::uint64_t seed, int nrows, int ncols, double* bad) {
+    Rng r{seed};
+    long long mism = 0;
+    for (int row = 0; row < nrows; ++row) {
+        const int ew = 1 + r.below(1060);
+        const double c = rand_double(r, ew, ew);
+        const double term = rand_double(r, ew + r.below(40), ew + 40);
+        const int deg = 1 + r.below(40);
+        Chain ch = make_chain(0.0, c);
+        double ref = 0.0;
+        int pos = 0;
+        const int self = r.below(ncols);
+        for (int q = 0; q <= deg; ++q) {
+            const int col = q == deg ? ncols : pos + r.below((ncols - pos) / (deg - q + 1) * 2 + 1);
+            const int stop = col > ncols ? ncols : col;
+            const int L = stop - pos;
+            if (L > 0) {
+                ff_run(ch, c, L);
+                ref = naive(ref, c, L);
+            }
+            if (stop >= ncols) break;
+            const double t = (stop == self) ? 1.0 : term;
+            ch.s = ch.s + t;
+            ref = ref + t;
+            pos = stop + 1;
+        }
+        if (std::memcmp(&ch.s, &ref, sizeof ref) != 0) {
+            if (mism == 0 && bad) {
+                bad[0] = c;
+                bad[1] = term;
+                bad[2] = row;
+            }
+            ++mism;
+        }
+    }
+    return mism;
+}
+
+
+// Prefix segments: P(L) for every L < n against the naive trajectory.
+long long fft_prefix(std::uint64_t seed, int ncases, int maxn, double* bad) {
+    Rng r{seed};
+    long long mism = 0;
+    int t[kPrefixCap];
+    double s0[kPrefixCap], inc[kPrefixCap];
+    for (int k = 0; k < ncases; ++k) {
+        const int ec = r.below(8) == 0 ? r.below(4) : 1 + r.below(1100);
+        const double c = rand_double(r, ec, ec);
+        const int n = 1 + rand_len(r, maxn);
+        int count = 0, t_end = 0;
+        double s_end = 0.0;
+        build_prefix(c, n, t, s0, inc, &count, &t_end, &s_end);
+        double ref = 0.0;
+        for (int L = 0; L < n; ++L) {
+            double got;
+            if (L < t_end) {
+                got = prefix_value(t, s0, inc, count, L);
+            } else {
+                Chain ch = make_chain(s_end, c);
+                ff_run(ch, c, L - t_end);
+                got = ch.s;
+            }
+            if (std::memcmp(&got, &ref, sizeof ref) != 0) {
+                if (mism == 0 && bad) {
+                    bad[0] = c;
+                    bad[1] = n;
+                    bad[2] = L;
+                }
+                ++mism;
+                break;
+            }
+            ref = ref + c;
+        }
+    }
+    return mism;
+}
+
+// Two chains (num with p = W^2 e, den with e) through ff_run2, first run via
+// the prefix table, exactly as the kernel walks a row.
+long long fft_rows2(std::uint64_t seed, int nrows, int ncols, double* bad) {
+    Rng r{seed};
+    long long mism = 0;
+    int tp[2][kPrefixCap];
+    double sp[2][kPrefixCap], ip[2][kPrefixCap];
+    for (int row = 0; row < nrows; ++row) {
+        const int ew = 1 + r.below(1060);
+        const double e = rand_double(r, ew, ew);
+        const double p = 100.0 * e;
+        const double te = rand_double(r, ew + r.below(40), ew + 40);
+        const double tpv = 1.0 * te;
+        int cnt[2], tend[2];
+        double send[2];
+        build_prefix(p, ncols, tp[0], sp[0], ip[0], &cnt[0], &tend[0], &send[0]);
+        build_prefix(e, ncols, tp[1], sp[1], ip[1], &cnt[1], &tend[1], &send[1]);
+        const int deg = 1 + r.below(40);
+        const int self = r.below(ncols);
+        Chain num = make_chain(0.0, p), den = make_chain(0.0, e);
+        double rn = 0.0, rd = 0.0;
+        int pos = 0;
+        bool first = true;
+        for (int q = 0; q <= deg; ++q) {
+            int col = q == deg ? ncols : pos + r.below((ncols - pos) / (deg - q + 1) * 2 + 1);
+            if (col > ncols) col = ncols;
+            const int L = col - pos;
+            if (L > 0) {
+                if (first) {
+                    if (L < tend[0]) num.s = prefix_value(tp[0], sp[0], ip[0], cnt[0], L);
+                    else { num.s = send[0]; ff_run(num, p, L - tend[0]); }
+                    if (L < tend[1]) den.s = prefix_value(tp[1], sp[1], ip[1], cnt[1], L);
+                    else { den.s = send[1]; ff_run(den, e, L - tend[1]); }
+                    num.top = 0.0;
+                    den.top = 0.0;
+                } else {
+                    ff_run2(num, p, den, e, L);
+                }
+                rn = naive(rn, p, L);
+                rd = naive(rd, e, L);
+            }
+            first = false;
+            if (col >= ncols) break;
+            if (col == self) {
+                den.s = den.s + 1.0;
+                rd = rd + 1.0;
+            } else {
+                num.s = num.s + tpv;
+                den.s = den.s + te;
+                rn = rn + tpv;
+                rd = rd + te;
+            }
+            pos = col + 1;
+        }
+        if (std::memcmp(&num.s, &rn, sizeof rn) != 0 || std::memcmp(&den.s, &rd, sizeof rd) != 0) {
+            if (mism == 0 && bad) {
+                bad[0] = e;
+                bad[1] = te;
+                bad[2] = row;
+            }
+            ++mism;
+        }
+    }
+    return mism;
+}
+
+double fft_run(double s, double c, int L) {
+    Chain ch = make_chain(s, c);
+    ff_run(ch, c, L);
+    return ch.s;
+}
+
+double fft_naive(double s, double c, long long L) { return naive(s, c, L); }
+
+}  // extern "C"
