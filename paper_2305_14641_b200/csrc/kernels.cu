@@ -15,6 +15,8 @@
 // (ff_chain below), which reproduces the sequential result bit for bit.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include <cub/device/device_scan.cuh>
 
 #include "gqc_internal.h"
@@ -23,6 +25,7 @@ namespace gqc {
 namespace {
 
 constexpr int kBlock = 256;
+constexpr int kWarpKernelMinSigma = 8;  // below this, thread-per-(row, sigma)
 
 
 #include "ff_chain.cuh"
@@ -254,6 +257,159 @@ __global__ void __launch_bounds__(kBlock) potential_kernel(const __grid_constant
 }
 
 // ---------------------------------------------------------------------------
+// Warp-per-row potential kernel (n_sigma >= 8): lane s of a warp is sigma s of
+// one row, so the whole walk (breakpoints, run lengths, neighbour terms) is
+// warp-uniform and only the fast-forward arithmetic differs between lanes.
+// The row's neighbour ids are loaded 32 at a time with one coalesced load and
+// read back with shuffles; the prefix search keys live in shared memory.
+// Persistent: each warp strides over rows.
+// ---------------------------------------------------------------------------
+constexpr int kPrefixStride = kPrefixCap + 1;  // padded: no bank conflicts across lanes
+
+template <bool kFF, int kW>
+__global__ void __launch_bounds__(kBlock) potential_warp_kernel(const __grid_constant__ PotentialLaunch P,
+                                                                const PrefixTable T) {
+    __shared__ double sc[kSigmaFields][kMaxSigmaPerLaunch];
+    __shared__ int pt[kFF ? 2 * kMaxSigmaPerLaunch * kPrefixStride : 1];
+    __shared__ int pcount[2 * kMaxSigmaPerLaunch], pend[2 * kMaxSigmaPerLaunch];
+    const int S = P.n_sigma;
+    for (int idx = threadIdx.x; idx < kSigmaFields * kMaxSigmaPerLaunch; idx += blockDim.x) {
+        const int ss = idx % kMaxSigmaPerLaunch, f = idx / kMaxSigmaPerLaunch;
+        if (ss < S) sc[f][ss] = reinterpret_cast<const double*>(&P.c[ss])[f];
+    }
+    if constexpr (kFF) {
+        for (int idx = threadIdx.x; idx < 2 * S * kPrefixCap; idx += blockDim.x) {
+            const int q = idx / kPrefixCap, j = idx % kPrefixCap;
+            pt[q * kPrefixStride + j] = T.t[idx];
+        }
+        for (int q = threadIdx.x; q < 2 * S; q += blockDim.x) {
+            pcount[q] = T.count[q];
+            pend[q] = T.t_end[q];
+        }
+    }
+    __syncthreads();
+
+    constexpr unsigned kFull = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int s = min(lane, S - 1);  // lanes >= S shadow the last sigma (uniform walk)
+    const double pW = sc[3][s], eW = sc[2][s], e1 = sc[4][s], p1 = sc[5][s];
+    const int tie_num = tie_binade(pW), tie_den = tie_binade(eW);
+    const int n = P.n;
+    const bool tail = P.tail != 0;
+    const long long warps = static_cast<long long>(gridDim.x) * (kBlock / 32);
+
+    // W run of L columns starting at column pos (the first run, pos == 0,
+    // comes from the prefix table).
+    auto w_run = [&](Chain& num, Chain& den, const int pos, const int L) {
+        if (L <= 0) return;
+        if constexpr (kFF) {
+            if (pos == 0) {
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int q = 2 * s + c;
+                    Chain& ch = c ? den : num;
+                    if (L < pend[q]) {
+                        const int* tq = pt + q * kPrefixStride;
+                        int lo = 0, hi = pcount[q] - 1;
+                        while (lo < hi) {
+                            const int mid = (lo + hi + 1) >> 1;
+                            if (tq[mid] <= L) lo = mid;
+                            else hi = mid - 1;
+                        }
+                        ch.s = __fma_rn(static_cast<double>(L - tq[lo]), T.inc[q * kPrefixCap + lo],
+                                        T.s0[q * kPrefixCap + lo]);
+                    } else {
+                        ch.s = T.s_end[q];
+                        ff_run(ch, c ? eW : pW, L - pend[q]);
+                    }
+                    ch.top = 0.0;
+                }
+            } else {
+                ff_run2(num, pW, den, eW, L);
+            }
+        } else {
+            replay(num.s, den.s, pW, eW, L);
+        }
+    };
+
+    for (long long row = P.row_begin + static_cast<long long>(blockIdx.x) * (kBlock / 32) + (threadIdx.x >> 5);
+         row < P.row_end; row += warps) {
+        const int i = static_cast<int>(row);
+        const long long kbeg = P.offsets[i], kend = P.offsets[i + 1];
+        Chain num, den;
+        num.s = 0.0; num.top = 0.0; num.inc = 0.0; num.f_tie = tie_num; num.flags = 0;
+        den.s = 0.0; den.top = 0.0; den.inc = 0.0; den.f_tie = tie_den; den.flags = 0;
+        int pos = 0;              // first column not yet added
+        bool self_pending = true;
+        // neighbours in chunks of 32: one coalesced load, then shuffles
+        for (long long base = kbeg; base < kend; base += 32) {
+            const int cnt = static_cast<int>(min(32ll, kend - base));
+            const int my = lane < cnt ? __ldg(P.nbr + base + lane) : n;
+            double myw = 1.0;
+            if constexpr (kW != kUnit) myw = lane < cnt ? __ldg(P.w + base + lane) : 1.0;
+            for (int j = 0; j < cnt; ++j) {
+                const int col = __shfl_sync(kFull, my, j);
+                if (self_pending && i < col) {  // the row's own column precedes this neighbour
+                    w_run(num, den, pos, i - pos);
+                    den.s = __dadd_rn(den.s, 1.0);  // self: num += 0, den += 1
+                    pos = i + 1;
+                    self_pending = false;
+                }
+                w_run(num, den, pos, col - pos);
+                const bool at_tail = tail && col == n - 1;
+                double e, p;
+                if constexpr (kW == kUnit) {
+                    e = at_tail ? sc[8][s] : e1;
+                    p = at_tail ? sc[9][s] : p1;
+                } else {
+                    const double wk = __shfl_sync(kFull, myw, j);
+                    const double d2 = __dmul_rn(wk, wk);
+                    if constexpr (kW == kEntryTable) {
+                        e = __ldg(P.entry_exp + (base + j) * P.entry_ld + P.entry_col0 + s);
+                    } else {
+                        if (at_tail) {  // glibc value, stored in row n-1's entry order
+                            long long lo = P.offsets[n - 1], hi = P.offsets[n];
+                            const long long b0 = lo;
+                            while (lo < hi) {
+                                const long long mid = (lo + hi) >> 1;
+                                if (__ldg(P.nbr + mid) < i) lo = mid + 1;
+                                else hi = mid;
+                            }
+                            e = __ldg(P.tail_exp + (lo - b0) * S + s);
+                        } else {
+                            e = pexp_dev(__dmul_rn(sc[1][s], d2));
+                        }
+                    }
+                    p = __dmul_rn(d2, e);
+                }
+                num.s = __dadd_rn(num.s, p);
+                den.s = __dadd_rn(den.s, e);
+                pos = col + 1;
+            }
+        }
+        if (self_pending) {
+            w_run(num, den, pos, i - pos);
+            den.s = __dadd_rn(den.s, 1.0);
+            pos = i + 1;
+        }
+        // final run [pos, n); the Eigen scalar tail column n-1 uses glibc constants
+        const int L = n - pos;
+        if (L > 0) {
+            if (tail) {
+                w_run(num, den, pos, L - 1);
+                num.s = __dadd_rn(num.s, sc[7][s]);
+                den.s = __dadd_rn(den.s, sc[6][s]);
+            } else {
+                w_run(num, den, pos, L);
+            }
+        }
+        if (lane < S)
+            P.out[static_cast<long long>(i - P.row_begin) * P.out_ld + P.out_col0 + lane] =
+                __dmul_rn(sc[0][s], __ddiv_rn(num.s, den.s));
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K3: successor = lexicographic (v, id) argmin over the closed neighbourhood
 // (ggd.cpp:7-24). Thread = (row, sigma), sigma fastest: a neighbour's
 // potentials for all sigmas are one contiguous node-major line.
@@ -408,19 +564,46 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
         prefix_kernel<<<1, 64, 0, st>>>(p, T);
         count_launch();
     }
-    switch (p.weight_mode) {
-        case kUnit:
-            if (ff) potential_kernel<true, kUnit><<<grid, kBlock, 0, st>>>(p, T);
-            else potential_kernel<false, kUnit><<<grid, kBlock, 0, st>>>(p, T);
-            break;
-        case kDevicePexp:
-            if (ff) potential_kernel<true, kDevicePexp><<<grid, kBlock, 0, st>>>(p, T);
-            else potential_kernel<false, kDevicePexp><<<grid, kBlock, 0, st>>>(p, T);
-            break;
-        default:
-            if (ff) potential_kernel<true, kEntryTable><<<grid, kBlock, 0, st>>>(p, T);
-            else potential_kernel<false, kEntryTable><<<grid, kBlock, 0, st>>>(p, T);
-            break;
+    if (p.n_sigma >= kWarpKernelMinSigma) {
+        // persistent warp-per-row kernel: enough warps to fill every SM
+        static int num_sms = 0;
+        if (!num_sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        const long long rows = p.row_end - p.row_begin;
+        const long long want = (rows + kBlock / 32 - 1) / (kBlock / 32);
+        const dim3 wgrid(static_cast<unsigned>(std::min<long long>(want, static_cast<long long>(num_sms) * 8)));
+        switch (p.weight_mode) {
+            case kUnit:
+                if (ff) potential_warp_kernel<true, kUnit><<<wgrid, kBlock, 0, st>>>(p, T);
+                else potential_warp_kernel<false, kUnit><<<wgrid, kBlock, 0, st>>>(p, T);
+                break;
+            case kDevicePexp:
+                if (ff) potential_warp_kernel<true, kDevicePexp><<<wgrid, kBlock, 0, st>>>(p, T);
+                else potential_warp_kernel<false, kDevicePexp><<<wgrid, kBlock, 0, st>>>(p, T);
+                break;
+            default:
+                if (ff) potential_warp_kernel<true, kEntryTable><<<wgrid, kBlock, 0, st>>>(p, T);
+                else potential_warp_kernel<false, kEntryTable><<<wgrid, kBlock, 0, st>>>(p, T);
+                break;
+        }
+    } else {
+        switch (p.weight_mode) {
+            case kUnit:
+                if (ff) potential_kernel<true, kUnit><<<grid, kBlock, 0, st>>>(p, T);
+                else potential_kernel<false, kUnit><<<grid, kBlock, 0, st>>>(p, T);
+                break;
+            case kDevicePexp:
+                if (ff) potential_kernel<true, kDevicePexp><<<grid, kBlock, 0, st>>>(p, T);
+                else potential_kernel<false, kDevicePexp><<<grid, kBlock, 0, st>>>(p, T);
+                break;
+            default:
+                if (ff) potential_kernel<true, kEntryTable><<<grid, kBlock, 0, st>>>(p, T);
+                else potential_kernel<false, kEntryTable><<<grid, kBlock, 0, st>>>(p, T);
+                break;
+        }
     }
     count_launch();
     cudaError_t e = cudaGetLastError();
