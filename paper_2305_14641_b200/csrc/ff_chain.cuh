@@ -180,34 +180,42 @@ GQC_HD inline void ff_run(Chain& ch, const double c, int L) {
     }
 }
 
-// One step of the convergent two-chain loop for a chain with Lx adds left:
-// the whole remainder if it stays in the binade (one exact fma; inc == 0 is
+// One pass over a run of L > 0 adds that handles up to one binade crossing
+// inline: the whole run if it stays in the binade (one exact fma; inc == 0 is
 // the fixed point t == s), else the maximal in-binade jump plus the crossing
-// add, else (c >= base/2, or a half-ulp tie at odd s) one real add. Written
-// as selects so the lanes of a warp stay converged whatever case each lane
-// is in.
-GQC_HD inline void ff_step(Chain& ch, const double c, int& Lx) {
+// add (or a single real add when c >= base/2 or at a half-ulp tie with odd
+// s), then the remainder in the new binade if it fits there. Leaves L > 0
+// only for runs that cross more than one binade.
+GQC_HD inline void ff_pass(Chain& ch, const double c, int& L) {
     if (!(ch.s < ch.top)) refresh(ch, c);
     const bool ok = settled(ch);
-    const double t = gqc_fma(static_cast<double>(Lx), ch.inc, ch.s);
+    const double t = gqc_fma(static_cast<double>(L), ch.inc, ch.s);
     if (ok && t < ch.top) {
         ch.s = t;
-        Lx = 0;
+        L = 0;
         return;
     }
-    double m = 0.0;
-    if (ok) m = max_steps(ch, room_of(ch));
+    const double m = ok ? max_steps(ch, room_of(ch)) : 0.0;
     ch.s = gqc_add(gqc_fma(m, ch.inc, ch.s), c);
-    Lx -= static_cast<int>(m) + 1;
+    L -= static_cast<int>(m) + 1;
+    if (L <= 0) return;
+    refresh(ch, c);  // idempotent when the real add stayed in the binade
+    const double t2 = gqc_fma(static_cast<double>(L), ch.inc, ch.s);
+    if (settled(ch) && t2 < ch.top) {
+        ch.s = t2;
+        L = 0;
+    }
 }
 
-// Both chains of a W run of length L, advanced together until both are done.
+// Both chains of a W run of length L > 0: one pass each (independent, so the
+// two dependency chains interleave), then the general loop for the rare runs
+// that cross several binades.
 GQC_HD inline void ff_run2(Chain& a, const double ca, Chain& b, const double cb, const int L) {
     int La = L, Lb = L;
-    do {
-        if (La > 0) ff_step(a, ca, La);
-        if (Lb > 0) ff_step(b, cb, Lb);
-    } while (La > 0 || Lb > 0);
+    ff_pass(a, ca, La);
+    ff_pass(b, cb, Lb);
+    if (La > 0) ff_run(a, ca, La);
+    if (Lb > 0) ff_run(b, cb, Lb);
 }
 
 // ---------------------------------------------------------------------------

@@ -26,6 +26,8 @@ namespace {
 
 constexpr int kBlock = 256;
 constexpr int kWarpKernelMinSigma = 8;  // below this, thread-per-(row, sigma)
+// 4 x 256 threads per SM (<= 64 registers): measured best on B200 (vs 3 or 5)
+constexpr int kWarpKernelBlocksPerSM = 4;
 
 
 #include "ff_chain.cuh"
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(kBlock) potential_kernel(const __grid_constant
 constexpr int kPrefixStride = kPrefixCap + 1;  // padded: no bank conflicts across lanes
 
 template <bool kFF, int kW>
-__global__ void __launch_bounds__(kBlock) potential_warp_kernel(const __grid_constant__ PotentialLaunch P,
+__global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp_kernel(const __grid_constant__ PotentialLaunch P,
                                                                 const PrefixTable T) {
     __shared__ double sc[kSigmaFields][kMaxSigmaPerLaunch];
     __shared__ int pt[kFF ? 2 * kMaxSigmaPerLaunch * kPrefixStride : 1];
@@ -574,7 +576,10 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
         }
         const long long rows = p.row_end - p.row_begin;
         const long long want = (rows + kBlock / 32 - 1) / (kBlock / 32);
-        const dim3 wgrid(static_cast<unsigned>(std::min<long long>(want, static_cast<long long>(num_sms) * 8)));
+        // two resident waves of row-striding warps (the second wave evens out
+        // the power-law row costs; measured better than one wave)
+        const dim3 wgrid(static_cast<unsigned>(
+            std::min<long long>(want, static_cast<long long>(num_sms) * kWarpKernelBlocksPerSM * 2)));
         switch (p.weight_mode) {
             case kUnit:
                 if (ff) potential_warp_kernel<true, kUnit><<<wgrid, kBlock, 0, st>>>(p, T);
