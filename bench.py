@@ -41,7 +41,7 @@ UNIT = "GPairs/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["native", "reference"], default="native")
     ap.add_argument("--workload", choices=["lfr1m", "sbm100k", "rmat22"], default="lfr1m")
@@ -77,8 +77,10 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi clocks / throttle reasons sampled every 20 ms. Started before
+    the warm-up (nvidia-smi needs ~100 ms to emit its first sample) and
+    filtered to the timed window by timestamp."""
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -86,6 +88,7 @@ class ClockSampler:
         self.gpu = gpu_index
         self.proc = None
         self.path = None
+        self.window = None
 
     def start(self):
         fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
@@ -93,35 +96,61 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "-lms", "20"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+            return
+        t0 = time.time()
+        while time.time() - t0 < 3.0 and os.path.getsize(self.path) == 0:
+            time.sleep(0.02)
+
+    def mark(self, t_begin, t_end):
+        self.window = (t_begin, t_end)
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.05)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-        sm, smax, reasons = [], None, set()
+        import datetime
+        rows = []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 9:
+            if len(parts) < 10:
                 continue
             try:
-                sm.append(float(parts[1]))
-                smax = float(parts[2])
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(parts[2]), float(parts[3]),
+                             {nm for nm, v in zip(names, parts[6:10]) if v.lower() == "active"}))
             except ValueError:
                 continue
-            for nm, val in zip(names, parts[5:9]):
-                if val.lower() == "active":
-                    reasons.add(nm)
         os.unlink(self.path)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sel = rows
+        if self.window:
+            a, b = self.window
+            inside = [r for r in rows if a - 0.02 <= r[0] <= b + 0.02]
+            # a window shorter than the sampling period: take the samples bracketing it
+            sel = inside or sorted(rows, key=lambda r: abs(r[0] - (a + b) / 2))[:2]
+        reasons = set().union(*[r[3] for r in sel])
+        return {"sm_mhz": statistics.median(r[1] for r in sel), "sm_max_mhz": max(r[2] for r in sel),
+                "reasons": sorted(reasons), "samples": len(sel)}
+
+
+def recorded_traffic(kernel_key):
+    """DRAM bytes per launch of a kernel from the committed ncu capture
+    (profiles/traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p))[kernel_key]["dram_bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def measured_peaks():
@@ -168,13 +197,15 @@ def run_reference(args):
     sig = log_sigma_grid(W_DEFAULT, args.n_sigma)
     n = len(off) - 1
     threads = os.cpu_count() or 1
-    budget = 3.0
-    vals = []
+    budget = 2.0  # seconds of host work per step: (W + K) steps stay within a few minutes
+    vals, secs = [], []
     rows_used = 0
-    for it in range(args.warmup + args.steps):
+    warm = args.warmup
+    for it in range(warm + args.steps):
         pps, rows, el, _ = cpu_sample(off, nbr, sig, budget, threads)
-        if it >= args.warmup:
+        if it >= warm:
             vals.append(pps / 1e9)
+            secs.append(el)
             rows_used = len(rows)
     value = statistics.mean(vals)
     sample = (f"{rows_used} evenly strided rows x {len(sig)} sigmas per step "
@@ -182,10 +213,11 @@ def run_reference(args):
               "compute_potentials_parallel (Eigen pexp restated, ascending-j fp64)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(secs),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": desc, "n_nodes": n, "nnz": int(len(nbr)), "n_sigma": len(sig),
-                   "sigma_grid": "log_sigma_grid(10, 32)"},
+                   "sigma_grid": f"log_sigma_grid(10, {len(sig)})",
+                   "step": "one bounded row sample of the sweep (all sigmas), see cpu_baseline.sample"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -249,18 +281,19 @@ def run_native(args):
         launches[0] += N.last_launch_count()
         return V
 
+    sampler = ClockSampler(local)
+    sampler.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
 
     per_step, pot_ms, gather_ms, ggd_ms = [], [], [], []
-    sampler = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    sampler.start()
     launches[0] = 0
     t_wall = time.perf_counter()
+    t_epoch0 = time.time()
     for _ in range(args.steps):
         with torch.cuda.stream(stream):
             flush.zero_()  # L2 flush between timed steps, outside the step's events
@@ -278,6 +311,7 @@ def run_native(args):
         ggd_ms.append(ev["p2"].elapsed_time(e1))
     torch.cuda.synchronize(dev)
     wall = time.perf_counter() - t_wall
+    sampler.mark(t_epoch0, time.time())
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
@@ -326,8 +360,10 @@ def run_native(args):
                        "step": "potentials(all rows, all sigmas) + all-gather V + GGD(succ, centers, labels)"},
             "breakdown_ms": {"potentials": pot, "allgather": gat, "ggd": ggd, "wall_s_timed_region": wall},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": None,
-                         "kernel": "potential_kernel<FASTFWD,unit>",
+                         "frac": (achieved / peak) if achieved else None,
+                         "traffic": recorded_traffic("potential_warp_kernel<FASTFWD,unit>") if world == 1 else None,
+                         "traffic_source": "profiles/traffic.json (ncu --set full, LFR 1M, 32 sigmas)",
+                         "kernel": "potential_warp_kernel<FASTFWD,unit>",
                          "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
                          "note": "algorithmic bytes = 8(rows+1) + 4*nnz + 8*rows*S; the exact fast-forward is "
                                  "issue-bound (fp64/int chain arithmetic), see DESIGN.md"},

@@ -1,0 +1,15 @@
+#!/bin/bash
+# Full measurement pass on the GPU box (run from the repo root under gpurun):
+# build, GPU tests, smoke, bench (1 GPU), reference arm, ncu launch list and
+# full captures of the top kernels. Outputs land in gpurun_out/.
+set -x
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest_gpu=$?"
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke=$?"
+python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench=$?"
+python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "bench_ref=$?"
+python bench.py --profile --steps 1 --warmup 1 > gpurun_out/plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+    python bench.py --profile --steps 1 --warmup 1 > gpurun_out/ncu_launches.log 2>&1; echo "ncu_launches=$?"
+ncu --set full --clock-control none --import-source on -k regex:"potential_warp|successors_kernel" -s 2 -c 2 \
+    -o gpurun_out/prof_full python bench.py --profile --steps 1 --warmup 1 > gpurun_out/ncu_full.log 2>&1; echo "ncu_full=$?"
