@@ -14,7 +14,7 @@ LIBGQC    := $(PKG)/libgqc.so
 GQC_SRCS  := $(CSRC)/capi.cu $(CSRC)/kernels.cu $(CSRC)/host_exp.cpp
 GQC_HDRS  := include/gqc.h $(CSRC)/gqc_internal.h
 
-all: $(LIBGQC) oracle
+all: $(LIBGQC) oracle facade
 
 $(LIBGQC): $(GQC_SRCS) $(GQC_HDRS)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(GQC_SRCS) 2> $(PKG)/build_ptxas.log || (cat $(PKG)/build_ptxas.log; exit 1)
@@ -23,7 +23,26 @@ oracle:
 	$(MAKE) -s -C oracle
 
 clean:
-	rm -f $(LIBGQC) $(PKG)/build_ptxas.log
+	rm -f $(LIBGQC) $(PKG)/build_ptxas.log $(LIBFACADE) $(CLI)
 	$(MAKE) -s -C oracle clean
 
 .PHONY: all oracle clean
+
+# graphqc-compatible C++ host facade (reference API) + CLI, on top of libgqc.
+HOST      := $(PKG)/host
+LIBFACADE := $(PKG)/libgraphqc.so
+CLI       := $(PKG)/bin/graphqc
+HOSTFLAGS := -O2 -std=c++20 -ffp-contract=off -fPIC -Wall -Wextra -I $(HOST)/include -I include
+HOST_SRCS := $(wildcard $(HOST)/src/*.cpp)
+HOST_HDRS := $(wildcard $(HOST)/include/graphqc/*.hpp) $(HOST)/src/device.hpp include/gqc.h
+
+facade: $(LIBFACADE) $(CLI)
+
+$(LIBFACADE): $(HOST_SRCS) $(HOST_HDRS) $(LIBGQC)
+	$(CXX) $(HOSTFLAGS) -shared -o $@ $(HOST_SRCS) -L$(PKG) -lgqc -Wl,-rpath,'$$ORIGIN'
+
+$(CLI): $(HOST)/tools/graphqc_main.cpp $(LIBFACADE)
+	@mkdir -p $(PKG)/bin
+	$(CXX) $(HOSTFLAGS) -o $@ $< -L$(PKG) -lgraphqc -lgqc -Wl,-rpath,'$$ORIGIN/..'
+
+.PHONY: facade

@@ -1,0 +1,31 @@
+// graphqc-compatible host facade: Graph Gradient Descent (reference:
+// include/graphqc/ggd.hpp:15-37), on the GPU through the C-ABI.
+#pragma once
+
+#include <cstdint>
+#include <span>
+#include <vector>
+
+#include "graphqc/graph.hpp"
+#include "graphqc/potential.hpp"
+
+namespace graphqc {
+
+struct SuccessorMap {
+    std::vector<std::int32_t> succ;
+};
+
+struct ClusterAssignment {
+    std::vector<std::int32_t> center;
+    std::vector<std::int32_t> cluster_index;
+    std::vector<std::int32_t> centers;
+    std::int32_t num_clusters = 0;
+};
+
+SuccessorMap build_successors(const Graph& g, const PotentialField& pf);
+ClusterAssignment resolve_centers(const SuccessorMap& s);
+ClusterAssignment cluster(const Graph& g, double sigma, int workers = 1);
+// One assignment per sigma from one batched device sweep.
+std::vector<ClusterAssignment> cluster_batch(const Graph& g, std::span<const double> sigmas);
+
+}  // namespace graphqc
