@@ -381,23 +381,24 @@ def e2e_leg(args, N, torch, dist, off, nbr, sig, rank, world, dev, stream, begin
     n, S = len(off) - 1, len(sig)
     pin_off = torch.from_numpy(off).pin_memory()
     pin_nbr = torch.from_numpy(nbr).pin_memory()
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, min(args.steps, 10))
     if world == 1:
         csr = N.Csr(pin_off.numpy(), pin_nbr.numpy(), None, W_DEFAULT)
-        center = torch.empty((S, n), dtype=torch.int32).pin_memory().numpy()
         ci = torch.empty((S, n), dtype=torch.int32).pin_memory().numpy()
         k = np.zeros(S, np.int32)
         sarr = np.ascontiguousarray(sig)
-        N.cluster_sweep_raw(csr, sarr, center, ci, k)  # warm-up
+        # run_sweep's per-sigma result (sweep.cpp:50-57): cluster index + count per sigma
+        N.cluster_sweep_raw(csr, sarr, None, ci, k)  # warm-up
         times = []
         for _ in range(steps):
             t0 = time.perf_counter()
-            N.cluster_sweep_raw(csr, sarr, center, ci, k)  # gqc_cluster_sweep: H2D CSR, compute, D2H labels
+            N.cluster_sweep_raw(csr, sarr, None, ci, k)  # gqc_cluster_sweep: H2D CSR, compute, D2H labels
             times.append(time.perf_counter() - t0)
         t = statistics.mean(times)
         return {"value": float(n) * n * S / t / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(off.nbytes + nbr.nbytes),
-                "d2h_bytes_per_step": int(center.nbytes + ci.nbytes + k.nbytes),
-                "api": "gqc_cluster_sweep (C-ABI, host buffers)", "ms_per_step": t * 1e3}
+                "d2h_bytes_per_step": int(ci.nbytes + k.nbytes),
+                "api": "gqc_cluster_sweep (C-ABI, pinned host buffers; cluster_index + counts per sigma)",
+                "ms_per_step": t * 1e3}
     # multi-GPU: per rank, H2D of the CSR, its row shard, all-gather, GGD, D2H of its rows' labels
     from paper_2305_14641_b200 import sharded
     rows = end - begin

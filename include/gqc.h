@@ -99,8 +99,10 @@ gqc_status gqc_resolve_centers(int32_t n, const int32_t* succ, int32_t* center, 
                                int32_t* num_clusters);
 
 /* Full pipeline per sigma (potentials -> successors -> centers). Outputs are
- * sigma-major [n_sigma][n]; v_out and succ_out may be NULL. num_clusters_out
- * has n_sigma entries. */
+ * sigma-major [n_sigma][n]; v_out, succ_out and center_out may be NULL (a
+ * sweep needs only cluster_index and the counts). num_clusters_out has
+ * n_sigma entries. The CSR upload is pipelined under the potential launches
+ * and the label downloads under the GGD of the next sigma chunk. */
 gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out,
                              int32_t* succ_out, int32_t* center_out, int32_t* cluster_index_out,
                              int32_t* num_clusters_out);

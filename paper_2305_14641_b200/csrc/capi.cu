@@ -84,6 +84,8 @@ struct DevBuf {
 
 struct DeviceCtx {
     cudaStream_t stream = nullptr;
+    cudaStream_t copy = nullptr;   // host<->device copies overlapped with compute
+    cudaEvent_t ev[16] = {};
     cudaMemPool_t pool = nullptr;  // stream-ordered scratch that keeps its memory
     DevBuf off, nbr, w, v_nm, v_sm, succ, center, ci, nc, ws, tail, entry;
 };
@@ -98,7 +100,11 @@ DeviceCtx& ctx() {
     }
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     DeviceCtx& c = all[dev];
-    if (!c.stream) cuda_check(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    if (!c.stream) {
+        cuda_check(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        cuda_check(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking), "cudaStreamCreate");
+        for (auto& e : c.ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    }
     if (!c.pool) {
         cudaMemPoolProps props{};
         props.allocType = cudaMemAllocationTypePinned;
@@ -157,7 +163,7 @@ void host_exp_table(const double* d2, long long count, const std::vector<double>
 // (device), for a device-resident CSR. host_w: the same weights on the host
 // (only consulted for weighted graphs), or nullptr to fetch what is needed.
 void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S, int row_begin, int row_end,
-                    double* v_nm, const double* host_w, cudaStream_t st) {
+                    double* v_nm, const double* host_w, cudaStream_t st, const std::int64_t* host_off = nullptr) {
     const int n = g.n;
     const int mode = g_opt.exp_mode;
     const bool weighted = g.w != nullptr;
@@ -169,16 +175,24 @@ void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S,
     long long last_beg = 0, last_deg = 0;
     if (weighted && tail) {
         long long o[2];
-        cuda_check(cudaMemcpy(o, g.offsets + (n - 1), 2 * sizeof(long long), cudaMemcpyDeviceToHost), "copy offsets");
+        if (host_off) {
+            o[0] = host_off[n - 1];
+            o[1] = host_off[n];
+        } else {
+            cuda_check(cudaStreamSynchronize(st), "sync");
+            cuda_check(cudaMemcpy(o, g.offsets + (n - 1), 2 * sizeof(long long), cudaMemcpyDeviceToHost), "copy offsets");
+        }
         last_beg = o[0];
         last_deg = o[1] - o[0];
         last_w.resize(last_deg);
         if (last_deg > 0) {
-            if (host_w)
+            if (host_w) {
                 std::copy(host_w + last_beg, host_w + last_beg + last_deg, last_w.begin());
-            else
+            } else {
+                cuda_check(cudaStreamSynchronize(st), "sync");
                 cuda_check(cudaMemcpy(last_w.data(), g.w + last_beg, last_deg * sizeof(double), cudaMemcpyDeviceToHost),
                            "copy weights");
+            }
         }
     }
     if (weighted && mode == GQC_EXP_GLIBC) {
@@ -187,6 +201,7 @@ void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S,
         const double* hw = host_w;
         if (!hw) {
             tmp.resize(g.nnz);
+            cuda_check(cudaStreamSynchronize(st), "sync");
             if (g.nnz)
                 cuda_check(cudaMemcpy(tmp.data(), g.w, g.nnz * sizeof(double), cudaMemcpyDeviceToHost), "copy weights");
             hw = tmp.data();
@@ -366,7 +381,7 @@ gqc_status gqc_build_successors(const gqc_csr* g, const double* v, int32_t* succ
         double* dv = C.v_nm.get<double>(g->n);
         int* ds = C.succ.get<int>(g->n);
         cuda_check(cudaMemcpyAsync(dv, v, g->n * sizeof(double), cudaMemcpyHostToDevice, st), "copy V");
-        cuda_check(launch_successors(g->n, d.offsets, d.nbr, dv, 1, ds, st), "successor kernel");
+        cuda_check(launch_successors(g->n, d.offsets, d.nbr, dv, 1, 0, 1, ds, st), "successor kernel");
         cuda_check(cudaMemcpyAsync(succ, ds, g->n * sizeof(int), cudaMemcpyDeviceToHost, st), "copy succ");
         cuda_check(cudaStreamSynchronize(st), "build successors");
     });
@@ -405,36 +420,87 @@ gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_s
     return guarded([&] {
         check_sigmas(sigmas, n_sigma);
         check_csr_shape(g);
-        if (!center_out || !cluster_index_out || !num_clusters_out) fail(GQC_EINVAL, "null output");
+        if (!cluster_index_out || !num_clusters_out) fail(GQC_EINVAL, "null output");
+        if (g->offsets[0] != 0 || g->offsets[g->n] != g->nnz) fail(GQC_EINVAL, "CSR offsets do not match nnz");
         DeviceCtx& C = ctx();
-        cudaStream_t st = C.stream;
-        const double* hw = nullptr;
-        gqc_csr d = upload_csr(C, g, st, &hw);
+        cudaStream_t st = C.stream, cs = C.copy;
         const int n = g->n;
+        const long long nnz = g->nnz;
+        const bool weighted = g->w && !all_unit(g->w, nnz);
+
+        // Pipeline: the CSR goes up in row slabs on the copy stream while the
+        // compute stream runs the potentials of the slabs already resident
+        // (rows are independent); GGD then runs in sigma chunks whose labels
+        // go down on the copy stream while the next chunk computes.
+        gqc_csr d = *g;
+        auto* off = C.off.get<std::int64_t>(n + 1);
+        auto* nbr = C.nbr.get<std::int32_t>(std::max<long long>(nnz, 1));
+        double* w = weighted ? C.w.get<double>(std::max<long long>(nnz, 1)) : nullptr;
+        d.offsets = off;
+        d.nbr = nbr;
+        d.w = w;
+        cuda_check(cudaMemcpyAsync(off, g->offsets, (n + 1) * sizeof(std::int64_t), cudaMemcpyHostToDevice, cs),
+                   "copy offsets");
+        const int slabs = nnz >= (1 << 20) ? 4 : 1;
+        std::vector<int> bound(slabs + 1, n);
+        bound[0] = 0;
+        for (int k = 1; k < slabs; ++k)  // equal-nnz row slabs
+            bound[k] = static_cast<int>(std::lower_bound(g->offsets, g->offsets + n + 1, nnz * k / slabs) - g->offsets);
         const std::size_t cells = static_cast<std::size_t>(n) * n_sigma;
         double* v_nm = C.v_nm.get<double>(cells);
-        run_potentials(C, d, sigmas, n_sigma, 0, n, v_nm, hw, st);
+        for (int k = 0; k < slabs; ++k) {
+            const long long a = g->offsets[bound[k]], b = g->offsets[bound[k + 1]];
+            if (b > a) {
+                cuda_check(cudaMemcpyAsync(nbr + a, g->nbr + a, (b - a) * sizeof(std::int32_t), cudaMemcpyHostToDevice, cs),
+                           "copy nbr");
+                if (weighted)
+                    cuda_check(cudaMemcpyAsync(w + a, g->w + a, (b - a) * sizeof(double), cudaMemcpyHostToDevice, cs),
+                               "copy weights");
+            }
+            cuda_check(cudaEventRecord(C.ev[k], cs), "event");
+            cuda_check(cudaStreamWaitEvent(st, C.ev[k], 0), "wait");
+            if (bound[k + 1] > bound[k])
+                run_potentials(C, d, sigmas, n_sigma, bound[k], bound[k + 1], v_nm + static_cast<std::size_t>(bound[k]) * n_sigma,
+                               weighted ? g->w : nullptr, st, g->offsets);
+        }
+        if (v_out) {  // sigma-major copy of the field
+            double* src = v_nm;
+            if (n_sigma > 1) {
+                src = C.v_sm.get<double>(cells);
+                cuda_check(launch_transpose(v_nm, n, n_sigma, src, st), "transpose");
+            }
+            cuda_check(cudaEventRecord(C.ev[8], st), "event");
+            cuda_check(cudaStreamWaitEvent(cs, C.ev[8], 0), "wait");
+            cuda_check(cudaMemcpyAsync(v_out, src, cells * sizeof(double), cudaMemcpyDeviceToHost, cs), "copy V");
+        }
         int* ds = C.succ.get<int>(cells);
         int* dc = C.center.get<int>(cells);
         int* dci = C.ci.get<int>(cells);
         int* dnc = C.nc.get<int>(n_sigma);
         const std::size_t wsb = labels_workspace_bytes(n, n_sigma);
         void* ws = C.ws.get<char>(wsb);
-        cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, ds, st), "successor kernel");
-        cuda_check(launch_chase(n, n_sigma, ds, dc, st), "chase kernel");
-        cuda_check(launch_labels(n, n_sigma, dc, dci, dnc, ws, wsb, st), "label kernels");
-        if (v_out) {
-            double* src = v_nm;
-            if (n_sigma > 1) {
-                src = C.v_sm.get<double>(cells);
-                cuda_check(launch_transpose(v_nm, n, n_sigma, src, st), "transpose");
-            }
-            cuda_check(cudaMemcpyAsync(v_out, src, cells * sizeof(double), cudaMemcpyDeviceToHost, st), "copy V");
+        const int chunk = n_sigma > 16 ? 16 : n_sigma;
+        int ev_i = 9;
+        for (int s0 = 0; s0 < n_sigma; s0 += chunk) {
+            const int Sc = std::min(chunk, n_sigma - s0);
+            const std::size_t o = static_cast<std::size_t>(s0) * n, c = static_cast<std::size_t>(Sc) * n;
+            cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, s0, Sc, ds + o, st), "successor kernel");
+            cuda_check(launch_chase(n, Sc, ds + o, dc + o, st), "chase kernel");
+            cuda_check(launch_labels(n, Sc, dc + o, dci + o, dnc + s0, ws, wsb, st), "label kernels");
+            cudaEvent_t e = C.ev[ev_i];
+            ev_i = ev_i == 15 ? 9 : ev_i + 1;
+            cuda_check(cudaEventRecord(e, st), "event");
+            cuda_check(cudaStreamWaitEvent(cs, e, 0), "wait");
+            if (succ_out)
+                cuda_check(cudaMemcpyAsync(succ_out + o, ds + o, c * sizeof(int), cudaMemcpyDeviceToHost, cs), "copy succ");
+            if (center_out)
+                cuda_check(cudaMemcpyAsync(center_out + o, dc + o, c * sizeof(int), cudaMemcpyDeviceToHost, cs), "copy center");
+            cuda_check(cudaMemcpyAsync(cluster_index_out + o, dci + o, c * sizeof(int), cudaMemcpyDeviceToHost, cs),
+                       "copy cluster index");
+            cuda_check(cudaMemcpyAsync(num_clusters_out + s0, dnc + s0, Sc * sizeof(int), cudaMemcpyDeviceToHost, cs),
+                       "copy counts");
         }
-        if (succ_out) cuda_check(cudaMemcpyAsync(succ_out, ds, cells * sizeof(int), cudaMemcpyDeviceToHost, st), "copy");
-        cuda_check(cudaMemcpyAsync(center_out, dc, cells * sizeof(int), cudaMemcpyDeviceToHost, st), "copy center");
-        cuda_check(cudaMemcpyAsync(cluster_index_out, dci, cells * sizeof(int), cudaMemcpyDeviceToHost, st), "copy");
-        cuda_check(cudaMemcpyAsync(num_clusters_out, dnc, n_sigma * sizeof(int), cudaMemcpyDeviceToHost, st), "copy");
+        cuda_check(cudaStreamSynchronize(cs), "cluster sweep (copies)");
         cuda_check(cudaStreamSynchronize(st), "cluster sweep");
     });
 }
@@ -466,7 +532,7 @@ gqc_status gqc_dev_ggd(const gqc_csr* g, const double* v, int32_t n_sigma, int32
         if (workspace_bytes < labels_workspace_bytes(g->n, n_sigma)) fail(GQC_EINVAL, "workspace too small");
         auto st = static_cast<cudaStream_t>(stream);
         int* s = succ ? succ : center;  // the chase runs in place on center
-        cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, s, st), "successor kernel");
+        cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, s, st), "successor kernel");
         cuda_check(launch_chase(g->n, n_sigma, s, center, st), "chase kernel");
         cuda_check(launch_labels(g->n, n_sigma, center, cluster_index, num_clusters, workspace, workspace_bytes, st),
                    "label kernels");

@@ -25,7 +25,8 @@ struct ClusterAssignment {
 SuccessorMap build_successors(const Graph& g, const PotentialField& pf);
 ClusterAssignment resolve_centers(const SuccessorMap& s);
 ClusterAssignment cluster(const Graph& g, double sigma, int workers = 1);
-// One assignment per sigma from one batched device sweep.
-std::vector<ClusterAssignment> cluster_batch(const Graph& g, std::span<const double> sigmas);
+// One assignment per sigma from one batched device sweep. with_center = false
+// fills only cluster_index / num_clusters (all a sweep's metrics need).
+std::vector<ClusterAssignment> cluster_batch(const Graph& g, std::span<const double> sigmas, bool with_center = true);
 
 }  // namespace graphqc

@@ -39,7 +39,7 @@ ClusterAssignment resolve_centers(const SuccessorMap& s) {
     return out;
 }
 
-std::vector<ClusterAssignment> cluster_batch(const Graph& g, std::span<const double> sigmas) {
+std::vector<ClusterAssignment> cluster_batch(const Graph& g, std::span<const double> sigmas, bool with_center) {
     if (sigmas.empty()) return {};
     for (double s : sigmas)
         if (!(s > 0.0)) throw std::invalid_argument("sigma must be positive");
@@ -51,17 +51,19 @@ std::vector<ClusterAssignment> cluster_batch(const Graph& g, std::span<const dou
     std::vector<std::int32_t> center, ci, k;
     for (std::size_t q0 = 0; q0 < sigmas.size(); q0 += kChunk) {
         const std::size_t m = std::min(kChunk, sigmas.size() - q0);
-        center.resize(m * n);
+        center.resize(with_center ? m * n : 0);
         ci.resize(m * n);
         k.resize(m);
         detail::check(gqc_cluster_sweep(&c, sigmas.data() + q0, static_cast<std::int32_t>(m), nullptr, nullptr,
-                                        center.data(), ci.data(), k.data()));
+                                        with_center ? center.data() : nullptr, ci.data(), k.data()));
         for (std::size_t q = 0; q < m; ++q) {
             ClusterAssignment& a = out[q0 + q];
-            a.center.assign(center.begin() + q * n, center.begin() + (q + 1) * n);
             a.cluster_index.assign(ci.begin() + q * n, ci.begin() + (q + 1) * n);
             a.num_clusters = k[q];
-            a.centers = centers_of(a.center);
+            if (with_center) {
+                a.center.assign(center.begin() + q * n, center.begin() + (q + 1) * n);
+                a.centers = centers_of(a.center);
+            }
         }
     }
     return out;

@@ -229,7 +229,7 @@ def resolve_centers(succ: np.ndarray) -> ClusterAssignment:
     return ClusterAssignment(center, ci, int(k[0]))
 
 
-def cluster_sweep_raw(g: Csr, sigmas: np.ndarray, center: np.ndarray, ci: np.ndarray, k: np.ndarray,
+def cluster_sweep_raw(g: Csr, sigmas: np.ndarray, center: Optional[np.ndarray], ci: np.ndarray, k: np.ndarray,
                       v: Optional[np.ndarray] = None, succ: Optional[np.ndarray] = None):
     """gqc_cluster_sweep into caller-owned (e.g. pinned) sigma-major arrays."""
     cs = g.c_struct()
@@ -237,18 +237,23 @@ def cluster_sweep_raw(g: Csr, sigmas: np.ndarray, center: np.ndarray, ci: np.nda
                                   _ptr(ci), _ptr(k)))
 
 
-def cluster_sweep(g: Csr, sigmas: Sequence[float], want_v: bool = False, want_succ: bool = False):
+def cluster_sweep(g: Csr, sigmas: Sequence[float], want_v: bool = False, want_succ: bool = False,
+                  want_center: bool = True):
     """One ClusterAssignment per sigma (the per-sigma body of run_sweep,
-    sweep.cpp:50-57); optionally the potential fields and successor maps."""
+    sweep.cpp:50-57); optionally the potential fields and successor maps.
+    want_center=False skips the center arrays (centers still listed)."""
     s = np.ascontiguousarray(np.atleast_1d(np.asarray(sigmas, dtype=np.float64)))
     S, n = len(s), g.n
     v = np.empty((S, n)) if want_v else None
     succ = np.empty((S, n), dtype=np.int32) if want_succ else None
-    center = np.empty((S, n), dtype=np.int32)
+    center = np.empty((S, n), dtype=np.int32) if want_center else None
     ci = np.empty((S, n), dtype=np.int32)
     k = np.zeros(S, dtype=np.int32)
     cluster_sweep_raw(g, s, center, ci, k, v, succ)
-    out = [ClusterAssignment(center[q], ci[q], int(k[q])) for q in range(S)]
+    if center is None:
+        out = [ClusterAssignment(None, ci[q], int(k[q]), centers=np.zeros(0, np.int32)) for q in range(S)]
+    else:
+        out = [ClusterAssignment(center[q], ci[q], int(k[q])) for q in range(S)]
     return out, v, succ
 
 

@@ -270,3 +270,53 @@ def test_device_api_row_shards_assemble_to_full_field():
     assert np.array_equal(succ.cpu().numpy(), s_host)
     assert np.array_equal(center.cpu().numpy(), np.stack([r.center for r in res]))
     assert nc.cpu().tolist() == [r.num_clusters for r in res]
+
+
+def _dev_labels(g_csr, sig):
+    import torch
+    dg = N.DeviceCsr(g_csr)
+    S = len(sig)
+    v = torch.empty((g_csr.n, S), dtype=torch.float64, device="cuda")
+    N.dev_potentials(dg, sig, 0, g_csr.n, v)
+    succ = torch.empty((S, g_csr.n), dtype=torch.int32, device="cuda")
+    center, ci = torch.empty_like(succ), torch.empty_like(succ)
+    nc = torch.empty(S, dtype=torch.int32, device="cuda")
+    ws = torch.empty(N.dev_ggd_workspace(g_csr.n, S), dtype=torch.uint8, device="cuda")
+    N.dev_ggd(dg, v, S, succ, center, ci, nc, ws)
+    torch.cuda.synchronize()
+    return v.cpu().numpy().T.copy(), succ.cpu().numpy(), center.cpu().numpy(), ci.cpu().numpy(), nc.cpu().numpy()
+
+
+def test_pipelined_sweep_matches_device_path_sbm():
+    # >= 2^20 nnz: the host API uploads the CSR in 4 row slabs under the
+    # potential launches and downloads labels per 16-sigma chunk
+    off, nbr = H.sbm_csr()
+    csr = N.Csr(off, nbr, None, 10.0)
+    sig = O.log_sigma_grid(10.0, 32)
+    res, v, succ = N.cluster_sweep(csr, sig, want_v=True, want_succ=True)
+    vd, sd, cd, cid, ncd = _dev_labels(csr, sig)
+    assert_bits(v, vd)
+    assert np.array_equal(succ, sd)
+    assert np.array_equal(np.stack([r.center for r in res]), cd)
+    assert np.array_equal(np.stack([r.cluster_index for r in res]), cid)
+    assert [r.num_clusters for r in res] == ncd.tolist()
+    res2, _, _ = N.cluster_sweep(csr, sig, want_center=False)
+    assert np.array_equal(np.stack([r.cluster_index for r in res2]), cid)
+    assert [r.num_clusters for r in res2] == ncd.tolist()
+
+
+def test_pipelined_sweep_weighted_odd_n_sampled_oracle():
+    # weighted, odd N (Eigen tail column), > 2^20 entries: slabbed weights upload
+    n = 150_001
+    g = H.random_graph(n, 8.0, seed=21)
+    csr = g.csr(N)
+    sig = np.array([0.7, 2.3, 5.0, 11.0, 30.0])
+    res, v, succ = N.cluster_sweep(csr, sig, want_v=True, want_succ=True)
+    rows = np.arange(0, n, 1499, dtype=np.int32)
+    rows = np.append(rows, n - 1)
+    for q, s in enumerate(sig):
+        ref = O.potentials_rows(g.offsets, g.nbr, g.wt, 10.0, s, rows, workers=8)
+        assert_bits(v[q][rows], ref)
+    vd, sd, cd, cid, ncd = _dev_labels(csr, sig)
+    assert_bits(v, vd)
+    assert np.array_equal(np.stack([r.cluster_index for r in res]), cid)
