@@ -441,6 +441,16 @@ gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_s
         d.w = w;
         cuda_check(cudaMemcpyAsync(off, g->offsets, (n + 1) * sizeof(std::int64_t), cudaMemcpyHostToDevice, cs),
                    "copy offsets");
+        {  // row n-1 first: rows adjacent to the Eigen tail column search its list (weighted graphs)
+            const long long a = g->offsets[n - 1], b = g->offsets[n];
+            if (b > a) {
+                cuda_check(cudaMemcpyAsync(nbr + a, g->nbr + a, (b - a) * sizeof(std::int32_t), cudaMemcpyHostToDevice, cs),
+                           "copy nbr");
+                if (weighted)
+                    cuda_check(cudaMemcpyAsync(w + a, g->w + a, (b - a) * sizeof(double), cudaMemcpyHostToDevice, cs),
+                               "copy weights");
+            }
+        }
         const int slabs = nnz >= (1 << 20) ? 4 : 1;
         std::vector<int> bound(slabs + 1, n);
         bound[0] = 0;

@@ -219,3 +219,25 @@ def test_weighted_graph_sweep_matches_oracle(tmp_path):
     assert code == 0, err
     s, m = O.run_sweep(path, None, steps=12)
     assert out_csv.read_text() == s and out == m
+
+
+SMALL_GRAPHS = ["karate_weighted", "les_miserables_weighted", "les_miserables", "florentine", "davis", "planted_4x32"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", SMALL_GRAPHS)
+def test_config2_small_graph_sweeps_match_oracle(tmp_path, name):
+    # BASELINE config 2 (substitutes): default 30-point log
+    # sweep 0.1W..3W on 1 B200, CSV and mutation line byte-identical to the oracle
+    path = os.path.join(ROOT, "tests", "golden", f"{name}.edges")
+    out_csv = tmp_path / "s.csv"
+    code, out, err = run("sweep", path, "--out", out_csv)
+    assert code == 0, err
+    s, m = O.run_sweep(path, None)
+    assert out_csv.read_text() == s and out == m
+    for sigma in (1.0, 2.5, 5.0):
+        a_csv = tmp_path / "a.csv"
+        code, out, err = run("cluster", path, "--sigma", sigma, "--out", a_csv)
+        assert code == 0, err
+        a, r = O.run_cluster(path, None, sigma)
+        assert a_csv.read_text() == a and out == r

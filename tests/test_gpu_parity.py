@@ -313,7 +313,8 @@ def test_pipelined_sweep_weighted_odd_n_sampled_oracle():
     sig = np.array([0.7, 2.3, 5.0, 11.0, 30.0])
     res, v, succ = N.cluster_sweep(csr, sig, want_v=True, want_succ=True)
     rows = np.arange(0, n, 1499, dtype=np.int32)
-    rows = np.append(rows, n - 1)
+    # plus every row adjacent to the tail column N-1 and the tail row itself
+    rows = np.unique(np.concatenate([rows, g.nbr[g.offsets[n - 1]:g.offsets[n]], [n - 1]])).astype(np.int32)
     for q, s in enumerate(sig):
         ref = O.potentials_rows(g.offsets, g.nbr, g.wt, 10.0, s, rows, workers=8)
         assert_bits(v[q][rows], ref)
