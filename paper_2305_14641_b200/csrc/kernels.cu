@@ -440,45 +440,6 @@ __global__ void __launch_bounds__(kBlock) successors_kernel(int n, const long lo
     succ_sm[static_cast<long long>(s) * n + i] = best;
 }
 
-// K3 for 8..32 sigmas: warp = one row, lane = sigma. The (v, id)
-// lexicographic minimum is order-independent, so the neighbours of a 32-id
-// chunk (one coalesced load) are scanned 8 at a time with all eight 256-byte
-// node-major gathers in flight before the compares.
-__global__ void __launch_bounds__(kBlock) successors_warp_kernel(int n, const long long* __restrict__ off,
-                                                                 const int* __restrict__ nbr,
-                                                                 const double* __restrict__ v, int ld, int s0,
-                                                                 int S, int* __restrict__ succ_sm) {
-    constexpr unsigned kFull = 0xffffffffu;
-    const long long warp = (static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= n) return;
-    const int i = static_cast<int>(warp);
-    const int s = s0 + min(lane, S - 1);
-    int best = i;
-    double vb = __ldg(v + static_cast<long long>(i) * ld + s);
-    const long long kend = off[i + 1];
-    for (long long base = off[i]; base < kend; base += 32) {
-        const int cnt = static_cast<int>(min(32ll, kend - base));
-        const int my = lane < cnt ? __ldg(nbr + base + lane) : i;
-        for (int j0 = 0; j0 < cnt; j0 += 8) {
-            int id[8];
-            double vv[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) id[u] = __shfl_sync(kFull, my, min(j0 + u, 31));
-#pragma unroll
-            for (int u = 0; u < 8; ++u) vv[u] = __ldg(v + static_cast<long long>(id[u]) * ld + s);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if (j0 + u < cnt && (vv[u] < vb || (vv[u] == vb && id[u] < best))) {
-                    best = id[u];
-                    vb = vv[u];
-                }
-            }
-        }
-    }
-    if (lane < S) succ_sm[static_cast<long long>(lane) * n + i] = best;
-}
-
 // K4: chase successors to their fixed point. center[] starts as a copy of
 // succ; every thread follows pointers through center[], which other threads
 // overwrite with roots as they finish (any value read is an ancestor, so the
@@ -661,19 +622,14 @@ int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nb
     // columns s0 .. s0+n_sigma of the node-major V (leading dimension ld) ->
     // sigma-major succ_sm[n_sigma][n]
     auto st = static_cast<cudaStream_t>(stream);
+    // thread = (row, sigma), sigma fastest: a neighbour's potentials for the
+    // chunk's sigmas are one contiguous node-major line
     for (int c0 = 0; c0 < n_sigma; c0 += 32) {
         const int Sc = std::min(32, n_sigma - c0);
-        if (Sc >= kWarpKernelMinSigma) {
-            const long long want = (static_cast<long long>(n) + kBlock / 32 - 1) / (kBlock / 32);
-            successors_warp_kernel<<<static_cast<unsigned>(want), kBlock, 0, st>>>(
-                n, reinterpret_cast<const long long*>(offsets), nbr, v, ld, s0 + c0, Sc,
-                succ_sm + static_cast<long long>(c0) * n);
-        } else {
-            const long long threads = static_cast<long long>(n) * Sc;
-            successors_kernel<<<grid_for(threads), kBlock, 0, st>>>(
-                n, reinterpret_cast<const long long*>(offsets), nbr, v, ld, s0 + c0, Sc,
-                succ_sm - static_cast<long long>(s0) * n);
-        }
+        const long long threads = static_cast<long long>(n) * Sc;
+        successors_kernel<<<grid_for(threads), kBlock, 0, st>>>(
+            n, reinterpret_cast<const long long*>(offsets), nbr, v, ld, s0 + c0, Sc,
+            succ_sm - static_cast<long long>(s0) * n);
         count_launch();
     }
     return cudaGetLastError();
