@@ -56,7 +56,8 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
 // GGD argmin for the sigma columns [s0, s0 + n_sigma) of a node-major V with
 // leading dimension ld; writes sigma-major succ_sm[n_sigma][n].
 int launch_successors(std::int32_t n, const std::int64_t* offsets, const std::int32_t* nbr, const double* v,
-                      std::int32_t ld, std::int32_t s0, std::int32_t n_sigma, std::int32_t* succ_sm, void* stream);
+                      std::int32_t ld, std::int32_t s0, std::int32_t n_sigma, std::int32_t* succ_sm, void* pool,
+                      void* stream);
 int launch_chase(std::int32_t n, std::int32_t n_sigma, const std::int32_t* succ_sm, std::int32_t* center_sm,
                  void* stream);
 int launch_labels(std::int32_t n, std::int32_t n_sigma, const std::int32_t* center_sm, std::int32_t* cluster_index_sm,

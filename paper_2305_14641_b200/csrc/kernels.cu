@@ -17,6 +17,7 @@
 
 #include <algorithm>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "gqc_internal.h"
@@ -103,6 +104,26 @@ struct PrefixTable {
     int* t_end;
     double* s_end;
 };
+
+// Longest-first dynamic row scheduling of the warp kernel: rows in
+// descending-degree order (one radix sort per launch), handed out to warps
+// through an atomic counter, so hub rows of skewed graphs start first and
+// no warp idles while another still owns a backlog.
+struct RowSched {
+    const int* order;  // row ids, heaviest first
+    int* counter;      // next position in `order` (zeroed per launch)
+};
+constexpr int kRowsPerGrab = 2;
+constexpr int kHeavyDegree = 1024;  // GGD argmin: rows above this degree use a block each
+
+__global__ void row_degree_kernel(const long long* __restrict__ off, int row_begin, int rows, int* __restrict__ deg,
+                                  int* __restrict__ id) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= rows) return;
+    const int i = row_begin + k;
+    deg[k] = static_cast<int>(off[i + 1] - off[i]);
+    id[k] = i;
+}
 
 __global__ void prefix_kernel(const __grid_constant__ PotentialLaunch P, PrefixTable T) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -271,7 +292,7 @@ constexpr int kPrefixStride = kPrefixCap + 1;  // padded: no bank conflicts acro
 
 template <bool kFF, int kW>
 __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp_kernel(const __grid_constant__ PotentialLaunch P,
-                                                                const PrefixTable T) {
+                                                                const PrefixTable T, const RowSched R) {
     __shared__ double sc[kSigmaFields][kMaxSigmaPerLaunch];
     __shared__ int pt[kFF ? 2 * kMaxSigmaPerLaunch * kPrefixStride : 1];
     __shared__ int pcount[2 * kMaxSigmaPerLaunch], pend[2 * kMaxSigmaPerLaunch];
@@ -299,8 +320,6 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
     const int tie_num = tie_binade(pW), tie_den = tie_binade(eW);
     const int n = P.n;
     const bool tail = P.tail != 0;
-    const long long warps = static_cast<long long>(gridDim.x) * (kBlock / 32);
-
     // W run of L columns starting at column pos (the first run, pos == 0,
     // comes from the prefix table).
     auto w_run = [&](Chain& num, Chain& den, const int pos, const int L) {
@@ -335,9 +354,19 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
         }
     };
 
-    for (long long row = P.row_begin + static_cast<long long>(blockIdx.x) * (kBlock / 32) + (threadIdx.x >> 5);
-         row < P.row_end; row += warps) {
-        const int i = static_cast<int>(row);
+    const int nrows = P.row_end - P.row_begin;
+    int grab = 0, left = 0;
+    for (;;) {
+        if (left == 0) {  // next batch of rows, heaviest first
+            int g0 = 0;
+            if (lane == 0) g0 = atomicAdd(R.counter, kRowsPerGrab);
+            grab = __shfl_sync(kFull, g0, 0);
+            if (grab >= nrows) break;
+            left = min(kRowsPerGrab, nrows - grab);
+        }
+        const int i = R.order[grab];
+        ++grab;
+        --left;
         const long long kbeg = P.offsets[i], kend = P.offsets[i + 1];
         Chain num, den;
         num.s = 0.0; num.top = 0.0; num.inc = 0.0; num.f_tie = tie_num; num.flags = 0;
@@ -426,9 +455,10 @@ __global__ void __launch_bounds__(kBlock) successors_kernel(int n, const long lo
     const long long i64 = tid / Sc;
     if (i64 >= n) return;
     const int i = static_cast<int>(i64);
+    const long long kend = off[i + 1];
+    if (kend - off[i] > kHeavyDegree) return;  // heavy rows: successors_heavy_kernel
     int best = i;
     double vb = __ldg(v + i64 * S + s);
-    const long long kend = off[i + 1];
     for (long long k = off[i]; k < kend; ++k) {
         const int j = __ldg(nbr + k);
         const double vj = __ldg(v + static_cast<long long>(j) * S + s);
@@ -438,6 +468,69 @@ __global__ void __launch_bounds__(kBlock) successors_kernel(int n, const long lo
         }
     }
     succ_sm[static_cast<long long>(s) * n + i] = best;
+}
+
+// Heavy rows (degree > kHeavyDegree, e.g. R-MAT hubs with ~10^5 neighbours):
+// one block per (heavy row, sigma) pair strides over the neighbour list and
+// reduces the lexicographic (v, id) minimum, which is associative, so a hub no
+// longer serialises on one thread. The heavy rows are listed by a marking pass.
+__global__ void mark_heavy_kernel(int n, const long long* __restrict__ off, int* __restrict__ list,
+                                  int* __restrict__ count) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && off[i + 1] - off[i] > kHeavyDegree) list[atomicAdd(count, 1)] = i;
+}
+
+__device__ __forceinline__ bool lex_less(double va, int ia, double vb, int ib) {
+    return va < vb || (va == vb && ia < ib);
+}
+
+__global__ void __launch_bounds__(kBlock) successors_heavy_kernel(const long long* __restrict__ off,
+                                                                  const int* __restrict__ nbr,
+                                                                  const double* __restrict__ v, int ld, int s0, int Sc,
+                                                                  int n, const int* __restrict__ list,
+                                                                  const int* __restrict__ count,
+                                                                  int* __restrict__ succ_sm) {
+    __shared__ double sv[kBlock / 32];
+    __shared__ int si[kBlock / 32];
+    const long long pairs = static_cast<long long>(*count) * Sc;
+    for (long long pq = blockIdx.x; pq < pairs; pq += gridDim.x) {
+        const int i = list[pq / Sc];
+        const int s = s0 + static_cast<int>(pq % Sc);
+        double vb = __ldg(v + static_cast<long long>(i) * ld + s);
+        int best = i;
+        const long long kend = off[i + 1];
+        for (long long k = off[i] + threadIdx.x; k < kend; k += kBlock) {
+            const int j = __ldg(nbr + k);
+            const double vj = __ldg(v + static_cast<long long>(j) * ld + s);
+            if (lex_less(vj, j, vb, best)) {
+                vb = vj;
+                best = j;
+            }
+        }
+#pragma unroll
+        for (int off2 = 16; off2 > 0; off2 >>= 1) {
+            const double ov = __shfl_down_sync(0xffffffffu, vb, off2);
+            const int oi = __shfl_down_sync(0xffffffffu, best, off2);
+            if (lex_less(ov, oi, vb, best)) {
+                vb = ov;
+                best = oi;
+            }
+        }
+        if ((threadIdx.x & 31) == 0) {
+            sv[threadIdx.x >> 5] = vb;
+            si[threadIdx.x >> 5] = best;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < kBlock / 32; ++w)
+                if (lex_less(sv[w], si[w], vb, best)) {
+                    vb = sv[w];
+                    best = si[w];
+                }
+            succ_sm[static_cast<long long>(s - s0) * n + i] = best;
+        }
+        __syncthreads();
+    }
 }
 
 // K4: chase successors to their fixed point. center[] starts as a copy of
@@ -568,33 +661,57 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
         count_launch();
     }
     if (p.n_sigma >= kWarpKernelMinSigma) {
-        // persistent warp-per-row kernel: enough warps to fill every SM
+        // persistent warp-per-row kernel: one resident wave, rows scheduled
+        // longest first through an atomic counter
         static int num_sms = 0;
         if (!num_sms) {
             int dev = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
         }
-        const long long rows = p.row_end - p.row_begin;
-        const long long want = (rows + kBlock / 32 - 1) / (kBlock / 32);
-        // two resident waves of row-striding warps (the second wave evens out
-        // the power-law row costs; measured better than one wave)
+        const int rows = p.row_end - p.row_begin;
+        auto pl = static_cast<cudaMemPool_t>(pool);
+        std::size_t sort_bytes = 0;
+        cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, static_cast<const int*>(nullptr),
+                                                  static_cast<int*>(nullptr), static_cast<const int*>(nullptr),
+                                                  static_cast<int*>(nullptr), rows);
+        const std::size_t arr = ((static_cast<std::size_t>(rows) * sizeof(int)) + 255) & ~static_cast<std::size_t>(255);
+        void* sched = nullptr;
+        cudaError_t e = cudaMallocFromPoolAsync(&sched, 4 * arr + sort_bytes + 256, pl, st);
+        if (e != cudaSuccess) return e;
+        char* b = static_cast<char*>(sched);
+        int* deg_in = reinterpret_cast<int*>(b);
+        int* deg_out = reinterpret_cast<int*>(b + arr);
+        int* id_in = reinterpret_cast<int*>(b + 2 * arr);
+        int* id_out = reinterpret_cast<int*>(b + 3 * arr);
+        int* counter = reinterpret_cast<int*>(b + 4 * arr);
+        void* temp = b + 4 * arr + 256;
+        row_degree_kernel<<<grid_for(rows), kBlock, 0, st>>>(reinterpret_cast<const long long*>(p.offsets),
+                                                              p.row_begin, rows, deg_in, id_in);
+        count_launch();
+        e = cub::DeviceRadixSort::SortPairsDescending(temp, sort_bytes, deg_in, deg_out, id_in, id_out, rows, 0, 32, st);
+        count_launch(2);
+        if (e != cudaSuccess) return e;
+        cudaMemsetAsync(counter, 0, sizeof(int), st);
+        const RowSched R{id_out, counter};
+        const long long want = (static_cast<long long>(rows) + kBlock / 32 - 1) / (kBlock / 32);
         const dim3 wgrid(static_cast<unsigned>(
-            std::min<long long>(want, static_cast<long long>(num_sms) * kWarpKernelBlocksPerSM * 2)));
+            std::min<long long>(want, static_cast<long long>(num_sms) * kWarpKernelBlocksPerSM)));
         switch (p.weight_mode) {
             case kUnit:
-                if (ff) potential_warp_kernel<true, kUnit><<<wgrid, kBlock, 0, st>>>(p, T);
-                else potential_warp_kernel<false, kUnit><<<wgrid, kBlock, 0, st>>>(p, T);
+                if (ff) potential_warp_kernel<true, kUnit><<<wgrid, kBlock, 0, st>>>(p, T, R);
+                else potential_warp_kernel<false, kUnit><<<wgrid, kBlock, 0, st>>>(p, T, R);
                 break;
             case kDevicePexp:
-                if (ff) potential_warp_kernel<true, kDevicePexp><<<wgrid, kBlock, 0, st>>>(p, T);
-                else potential_warp_kernel<false, kDevicePexp><<<wgrid, kBlock, 0, st>>>(p, T);
+                if (ff) potential_warp_kernel<true, kDevicePexp><<<wgrid, kBlock, 0, st>>>(p, T, R);
+                else potential_warp_kernel<false, kDevicePexp><<<wgrid, kBlock, 0, st>>>(p, T, R);
                 break;
             default:
-                if (ff) potential_warp_kernel<true, kEntryTable><<<wgrid, kBlock, 0, st>>>(p, T);
-                else potential_warp_kernel<false, kEntryTable><<<wgrid, kBlock, 0, st>>>(p, T);
+                if (ff) potential_warp_kernel<true, kEntryTable><<<wgrid, kBlock, 0, st>>>(p, T, R);
+                else potential_warp_kernel<false, kEntryTable><<<wgrid, kBlock, 0, st>>>(p, T, R);
                 break;
         }
+        cudaFreeAsync(sched, st);
     } else {
         switch (p.weight_mode) {
             case kUnit:
@@ -618,20 +735,38 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
 }
 
 int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nbr, const double* v, int ld, int s0,
-                      int n_sigma, std::int32_t* succ_sm, void* stream) {
+                      int n_sigma, std::int32_t* succ_sm, void* pool, void* stream) {
     // columns s0 .. s0+n_sigma of the node-major V (leading dimension ld) ->
     // sigma-major succ_sm[n_sigma][n]
     auto st = static_cast<cudaStream_t>(stream);
+    auto off = reinterpret_cast<const long long*>(offsets);
+    void* scratch = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync(&scratch, sizeof(int) * (static_cast<std::size_t>(n) + 64),
+                                            static_cast<cudaMemPool_t>(pool), st);
+    if (e != cudaSuccess) return e;
+    int* count = static_cast<int*>(scratch);
+    int* list = count + 32;
+    cudaMemsetAsync(count, 0, sizeof(int), st);
+    mark_heavy_kernel<<<grid_for(n), kBlock, 0, st>>>(n, off, list, count);
+    count_launch(2);
     // thread = (row, sigma), sigma fastest: a neighbour's potentials for the
     // chunk's sigmas are one contiguous node-major line
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
     for (int c0 = 0; c0 < n_sigma; c0 += 32) {
         const int Sc = std::min(32, n_sigma - c0);
         const long long threads = static_cast<long long>(n) * Sc;
         successors_kernel<<<grid_for(threads), kBlock, 0, st>>>(
-            n, reinterpret_cast<const long long*>(offsets), nbr, v, ld, s0 + c0, Sc,
-            succ_sm - static_cast<long long>(s0) * n);
-        count_launch();
+            n, off, nbr, v, ld, s0 + c0, Sc, succ_sm - static_cast<long long>(s0) * n);
+        successors_heavy_kernel<<<num_sms * 4, kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, n, list, count,
+                                                               succ_sm + static_cast<long long>(c0) * n);
+        count_launch(2);
     }
+    cudaFreeAsync(scratch, st);
     return cudaGetLastError();
 }
 

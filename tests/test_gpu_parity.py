@@ -321,3 +321,24 @@ def test_pipelined_sweep_weighted_odd_n_sampled_oracle():
     vd, sd, cd, cid, ncd = _dev_labels(csr, sig)
     assert_bits(v, vd)
     assert np.array_equal(np.stack([r.cluster_index for r in res]), cid)
+
+
+def test_hub_rows_heavy_argmin_and_scheduling():
+    # hubs above the heavy-row threshold (1024) take the block-parallel argmin
+    # and the longest-first row schedule; everything still matches the oracle
+    rng = np.random.default_rng(11)
+    n = 6001
+    u = [np.zeros(3000, np.int32), np.full(1500, 17, np.int32), rng.integers(0, n, 6000).astype(np.int32)]
+    v = [np.arange(1, 3001, dtype=np.int32), rng.choice(n, 1500, replace=False).astype(np.int32),
+         rng.integers(0, n, 6000).astype(np.int32)]
+    g = H.G(n, np.concatenate(u), np.concatenate(v))
+    sig = O.log_sigma_grid(10.0, 12)
+    res, V, succ = N.cluster_sweep(g.csr(N), sig, want_v=True, want_succ=True)
+    for q, s in enumerate(sig):
+        vo, so, co, cio, ko = O.cluster(g.offsets, g.nbr, g.wt, 10.0, s, workers=8)
+        assert_bits(V[q], vo)
+        assert np.array_equal(succ[q], so) and np.array_equal(res[q].cluster_index, cio) and res[q].num_clusters == ko
+    # single-sigma path (thread-per-row potential kernel) and build_successors
+    for s in (1.0, 5.0):
+        vo = O.potentials(g.offsets, g.nbr, g.wt, 10.0, s, workers=8)
+        assert np.array_equal(N.build_successors(g.csr(N), vo), O.build_successors(g.offsets, g.nbr, vo))
