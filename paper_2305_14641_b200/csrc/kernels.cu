@@ -114,7 +114,7 @@ struct RowSched {
     int* counter;      // next position in `order` (zeroed per launch)
 };
 constexpr int kRowsPerGrab = 2;
-constexpr int kHeavyDegree = 1024;  // GGD argmin: rows above this degree use a block each
+constexpr int kHeavyDegree = 128;  // GGD argmin: rows above this degree use a block each
 
 __global__ void row_degree_kernel(const long long* __restrict__ off, int row_begin, int rows, int* __restrict__ deg,
                                   int* __restrict__ id) {
@@ -490,16 +490,21 @@ __global__ void __launch_bounds__(kBlock) successors_heavy_kernel(const long lon
                                                                   int n, const int* __restrict__ list,
                                                                   const int* __restrict__ count,
                                                                   int* __restrict__ succ_sm) {
-    __shared__ double sv[kBlock / 32];
-    __shared__ int si[kBlock / 32];
-    const long long pairs = static_cast<long long>(*count) * Sc;
-    for (long long pq = blockIdx.x; pq < pairs; pq += gridDim.x) {
-        const int i = list[pq / Sc];
-        const int s = s0 + static_cast<int>(pq % Sc);
+    // one block per heavy row: lane = sigma, the 8 warps split the neighbour
+    // list (each neighbour's potentials are one coalesced node-major line),
+    // then the per-warp minima are combined per sigma in shared memory
+    constexpr int kWarps = kBlock / 32;
+    __shared__ double sv[kWarps][32];
+    __shared__ int si[kWarps][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int s = s0 + min(lane, Sc - 1);
+    const int heavy = *count;
+    for (int h = blockIdx.x; h < heavy; h += gridDim.x) {
+        const int i = list[h];
         double vb = __ldg(v + static_cast<long long>(i) * ld + s);
         int best = i;
         const long long kend = off[i + 1];
-        for (long long k = off[i] + threadIdx.x; k < kend; k += kBlock) {
+        for (long long k = off[i] + warp; k < kend; k += kWarps) {
             const int j = __ldg(nbr + k);
             const double vj = __ldg(v + static_cast<long long>(j) * ld + s);
             if (lex_less(vj, j, vb, best)) {
@@ -507,27 +512,16 @@ __global__ void __launch_bounds__(kBlock) successors_heavy_kernel(const long lon
                 best = j;
             }
         }
-#pragma unroll
-        for (int off2 = 16; off2 > 0; off2 >>= 1) {
-            const double ov = __shfl_down_sync(0xffffffffu, vb, off2);
-            const int oi = __shfl_down_sync(0xffffffffu, best, off2);
-            if (lex_less(ov, oi, vb, best)) {
-                vb = ov;
-                best = oi;
-            }
-        }
-        if ((threadIdx.x & 31) == 0) {
-            sv[threadIdx.x >> 5] = vb;
-            si[threadIdx.x >> 5] = best;
-        }
+        sv[warp][lane] = vb;
+        si[warp][lane] = best;
         __syncthreads();
-        if (threadIdx.x == 0) {
-            for (int w = 1; w < kBlock / 32; ++w)
-                if (lex_less(sv[w], si[w], vb, best)) {
-                    vb = sv[w];
-                    best = si[w];
+        if (warp == 0) {
+            for (int w = 1; w < kWarps; ++w)
+                if (lex_less(sv[w][lane], si[w][lane], vb, best)) {
+                    vb = sv[w][lane];
+                    best = si[w][lane];
                 }
-            succ_sm[static_cast<long long>(s - s0) * n + i] = best;
+            if (lane < Sc) succ_sm[static_cast<long long>(lane) * n + i] = best;
         }
         __syncthreads();
     }
@@ -762,7 +756,7 @@ int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nb
         const long long threads = static_cast<long long>(n) * Sc;
         successors_kernel<<<grid_for(threads), kBlock, 0, st>>>(
             n, off, nbr, v, ld, s0 + c0, Sc, succ_sm - static_cast<long long>(s0) * n);
-        successors_heavy_kernel<<<num_sms * 4, kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, n, list, count,
+        successors_heavy_kernel<<<num_sms * 8, kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, n, list, count,
                                                                succ_sm + static_cast<long long>(c0) * n);
         count_launch(2);
     }
