@@ -252,33 +252,49 @@ def run_native(args):
     rows = end - begin
 
     with torch.cuda.stream(stream):
-        shard = torch.zeros((block, S), dtype=torch.float64, device=dev)
-        full = torch.empty((world * block, S), dtype=torch.float64, device=dev) if world > 1 else None
-        succ = torch.empty((S, n), dtype=torch.int32, device=dev)
-        center = torch.empty_like(succ)
-        ci = torch.empty_like(succ)
+        center = torch.empty((S, n), dtype=torch.int32, device=dev)
+        ci = torch.empty_like(center)
         nc = torch.empty(S, dtype=torch.int32, device=dev)
-        ws = torch.empty(N.dev_ggd_workspace(n, S), dtype=torch.uint8, device=dev)
+        ws = torch.empty(N.dev_resolve_workspace(n, S), dtype=torch.uint8, device=dev)
         flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 512 MiB > 126 MB L2
     torch.cuda.synchronize(dev)
 
     launches = [0]
     ev = {}
 
-    def step(record=False):
-        if record:
-            ev["p0"].record(stream)
-        if rows > 0:
-            N.dev_potentials(dg, sig, begin, end, shard[:rows], stream)
-            launches[0] += N.last_launch_count()
-        if record:
-            ev["p1"].record(stream)
-        with torch.cuda.stream(stream):
-            V = sharded.gather_rows(shard, n, None, full) if world > 1 else shard[:n]
-        if record:
-            ev["p2"].record(stream)
-        N.dev_ggd(dg, V, S, succ, center, ci, nc, ws, stream)
+    def pot_rows(b, e, out):
+        N.dev_potentials(dg, sig, b, e, out, stream)
         launches[0] += N.last_launch_count()
+
+    def succ_rows(V, b, e, out):
+        N.dev_successors(dg, V, S, b, e, out, stream)
+        launches[0] += N.last_launch_count()
+
+    def resolve(succ):
+        N.dev_resolve(n, S, succ, center, ci, nc, ws, stream)
+        launches[0] += N.last_launch_count()
+
+    with torch.cuda.stream(stream):
+        sweep = sharded.ShardedSweep(n, S, rank, world, dev, pot_rows, succ_rows, resolve)
+    shard = sweep.shard_v
+
+    def step(record=False):
+        # potentials of own rows -> all-gather V -> GGD argmin of own rows ->
+        # all-gather succ -> centers / labels (sharded.ShardedSweep)
+        with torch.cuda.stream(stream):
+            if record:
+                ev["p0"].record(stream)
+            if rows > 0:
+                pot_rows(begin, end, sweep.shard_v[:rows])
+            if record:
+                ev["p1"].record(stream)
+            V = sharded.gather_rows(sweep.shard_v, n, None, sweep.full_v)
+            if record:
+                ev["p2"].record(stream)
+            succ = sweep.successors(V)
+            if record:
+                ev["p3"].record(stream)
+            sweep.resolve(succ)
         return V
 
     sampler = ClockSampler(local)
@@ -287,7 +303,7 @@ def run_native(args):
         step()
     torch.cuda.synchronize(dev)
 
-    per_step, pot_ms, gather_ms, ggd_ms = [], [], [], []
+    per_step, parts = [], {"potentials": [], "allgather_v": [], "successors_allgather_succ": [], "resolve": []}
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -299,16 +315,17 @@ def run_native(args):
             flush.zero_()  # L2 flush between timed steps, outside the step's events
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        for k in ("p0", "p1", "p2"):
+        for k in ("p0", "p1", "p2", "p3"):
             ev[k] = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         step(record=True)
         e1.record(stream)
         e1.synchronize()
         per_step.append(e0.elapsed_time(e1))
-        pot_ms.append(ev["p0"].elapsed_time(ev["p1"]))
-        gather_ms.append(ev["p1"].elapsed_time(ev["p2"]))
-        ggd_ms.append(ev["p2"].elapsed_time(e1))
+        parts["potentials"].append(ev["p0"].elapsed_time(ev["p1"]))
+        parts["allgather_v"].append(ev["p1"].elapsed_time(ev["p2"]))
+        parts["successors_allgather_succ"].append(ev["p2"].elapsed_time(ev["p3"]))
+        parts["resolve"].append(ev["p3"].elapsed_time(e1))
     torch.cuda.synchronize(dev)
     wall = time.perf_counter() - t_wall
     sampler.mark(t_epoch0, time.time())
@@ -317,12 +334,15 @@ def run_native(args):
     clocks = sampler.stop()
     gpu_launches = launches[0]
 
-    ms = statistics.mean(per_step)
-    stats = torch.tensor([ms, statistics.mean(pot_ms), statistics.mean(gather_ms), statistics.mean(ggd_ms)],
+    keys = list(parts)
+    stats = torch.tensor([statistics.mean(per_step)] + [statistics.mean(parts[k]) for k in keys],
                          dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
-    ms, pot, gat, ggd = stats.tolist()
+    vals = stats.tolist()
+    ms = vals[0]
+    breakdown = dict(zip(keys, vals[1:]))
+    pot = breakdown["potentials"]
     pairs = float(n) * n * S
     value = pairs / (ms / 1e3) / 1e9
 
@@ -358,7 +378,7 @@ def run_native(args):
                        "parallelism": f"row-shard x{world} + all-gather(V)",
                        "l2": "512 MiB write between timed steps (excluded from the per-step events)",
                        "step": "potentials(all rows, all sigmas) + all-gather V + GGD(succ, centers, labels)"},
-            "breakdown_ms": {"potentials": pot, "allgather": gat, "ggd": ggd, "wall_s_timed_region": wall},
+            "breakdown_ms": dict(breakdown, wall_s_timed_region=wall),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,
                          "traffic": recorded_traffic("potential_warp_kernel<FASTFWD,unit>") if world == 1 else None,

@@ -129,6 +129,18 @@ gqc_status gqc_dev_ggd(const gqc_csr* g, const double* v, int32_t n_sigma, int32
                        int32_t* cluster_index, int32_t* num_clusters, void* workspace, size_t workspace_bytes,
                        void* stream);
 
+/* Row-sharded GGD (multi-GPU): successors of rows [row_begin, row_end) from the
+ * full node-major V, written node-major succ_rows[(i - row_begin) * n_sigma + k]
+ * so equal row shards all-gather into one node-major succ[n][n_sigma]. */
+gqc_status gqc_dev_successors(const gqc_csr* g, const double* v, int32_t n_sigma, int32_t row_begin, int32_t row_end,
+                              int32_t* succ_rows, void* stream);
+
+/* Centers and dense cluster indices (sigma-major [n_sigma][n]) and counts from
+ * a node-major successor matrix succ_nm[n][n_sigma] built by gqc_dev_successors. */
+size_t gqc_dev_resolve_workspace(int32_t n, int32_t n_sigma);
+gqc_status gqc_dev_resolve(int32_t n, int32_t n_sigma, const int32_t* succ_nm, int32_t* center, int32_t* cluster_index,
+                           int32_t* num_clusters, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Node-major [n][n_sigma] -> sigma-major [n_sigma][n] transpose (device). */
 gqc_status gqc_dev_transpose(const double* v_nm, int32_t n, int32_t n_sigma, double* v_sm, void* stream);
 

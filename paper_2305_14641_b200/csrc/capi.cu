@@ -381,7 +381,7 @@ gqc_status gqc_build_successors(const gqc_csr* g, const double* v, int32_t* succ
         double* dv = C.v_nm.get<double>(g->n);
         int* ds = C.succ.get<int>(g->n);
         cuda_check(cudaMemcpyAsync(dv, v, g->n * sizeof(double), cudaMemcpyHostToDevice, st), "copy V");
-        cuda_check(launch_successors(g->n, d.offsets, d.nbr, dv, 1, 0, 1, ds, C.pool, st), "successor kernel");
+        cuda_check(launch_successors(g->n, d.offsets, d.nbr, dv, 1, 0, 1, 0, g->n, ds, 1, g->n, C.pool, st), "successor kernel");
         cuda_check(cudaMemcpyAsync(succ, ds, g->n * sizeof(int), cudaMemcpyDeviceToHost, st), "copy succ");
         cuda_check(cudaStreamSynchronize(st), "build successors");
     });
@@ -494,7 +494,7 @@ gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_s
         for (int s0 = 0; s0 < n_sigma; s0 += chunk) {
             const int Sc = std::min(chunk, n_sigma - s0);
             const std::size_t o = static_cast<std::size_t>(s0) * n, c = static_cast<std::size_t>(Sc) * n;
-            cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, s0, Sc, ds + o, C.pool, st), "successor kernel");
+            cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, s0, Sc, 0, n, ds + o, 1, n, C.pool, st), "successor kernel");
             cuda_check(launch_chase(n, Sc, ds + o, dc + o, st), "chase kernel");
             cuda_check(launch_labels(n, Sc, dc + o, dci + o, dnc + s0, ws, wsb, st), "label kernels");
             cudaEvent_t e = C.ev[ev_i];
@@ -543,9 +543,42 @@ gqc_status gqc_dev_ggd(const gqc_csr* g, const double* v, int32_t n_sigma, int32
         auto st = static_cast<cudaStream_t>(stream);
         DeviceCtx& C = ctx();
         int* s = succ ? succ : center;  // the chase runs in place on center
-        cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, s, C.pool, st), "successor kernel");
+        cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, 0, g->n, s, 1, g->n, C.pool, st), "successor kernel");
         cuda_check(launch_chase(g->n, n_sigma, s, center, st), "chase kernel");
         cuda_check(launch_labels(g->n, n_sigma, center, cluster_index, num_clusters, workspace, workspace_bytes, st),
+                   "label kernels");
+    });
+}
+
+gqc_status gqc_dev_successors(const gqc_csr* g, const double* v, int32_t n_sigma, int32_t row_begin, int32_t row_end,
+                              int32_t* succ_rows, void* stream) {
+    return guarded([&] {
+        check_csr_shape(g);
+        if (n_sigma < 1) fail(GQC_EINVAL, "sigma grid is empty");
+        if (row_begin < 0 || row_end > g->n || row_begin > row_end) fail(GQC_ERANGE, "row range out of range");
+        if (!v || (!succ_rows && row_end > row_begin)) fail(GQC_EINVAL, "null buffer");
+        DeviceCtx& C = ctx();
+        cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, row_begin, row_end, succ_rows,
+                                     n_sigma, 1, C.pool, static_cast<cudaStream_t>(stream)),
+                   "successor kernel");
+    });
+}
+
+size_t gqc_dev_resolve_workspace(int32_t n, int32_t n_sigma) {
+    if (n < 1 || n_sigma < 1) return 0;
+    return labels_workspace_bytes(n, n_sigma);
+}
+
+gqc_status gqc_dev_resolve(int32_t n, int32_t n_sigma, const int32_t* succ_nm, int32_t* center, int32_t* cluster_index,
+                           int32_t* num_clusters, void* workspace, size_t workspace_bytes, void* stream) {
+    return guarded([&] {
+        if (n < 1 || n_sigma < 1) fail(GQC_EINVAL, "empty input");
+        if (!succ_nm || !center || !cluster_index || !num_clusters || !workspace) fail(GQC_EINVAL, "null buffer");
+        if (workspace_bytes < labels_workspace_bytes(n, n_sigma)) fail(GQC_EINVAL, "workspace too small");
+        auto st = static_cast<cudaStream_t>(stream);
+        cuda_check(launch_transpose_i32(succ_nm, n, n_sigma, center, st), "transpose");
+        cuda_check(launch_chase(n, n_sigma, center, center, st), "chase kernel");
+        cuda_check(launch_labels(n, n_sigma, center, cluster_index, num_clusters, workspace, workspace_bytes, st),
                    "label kernels");
     });
 }

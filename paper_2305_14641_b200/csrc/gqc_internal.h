@@ -53,11 +53,15 @@ struct PotentialLaunch {
 // Stream-ordered scratch comes from `pool` (a cudaMemPool_t that keeps its
 // memory, so per-call scratch costs no driver allocation).
 int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* stream);
-// GGD argmin for the sigma columns [s0, s0 + n_sigma) of a node-major V with
-// leading dimension ld; writes sigma-major succ_sm[n_sigma][n].
+// GGD argmin for rows [row_begin, row_end) and the sigma columns
+// [s0, s0 + n_sigma) of a node-major V with leading dimension ld. Element
+// (row r of the range, sigma q) goes to out[r * out_row + q * out_col]
+// (sigma-major: out_row = 1, out_col = n; node-major shard: out_row = ld, out_col = 1).
 int launch_successors(std::int32_t n, const std::int64_t* offsets, const std::int32_t* nbr, const double* v,
-                      std::int32_t ld, std::int32_t s0, std::int32_t n_sigma, std::int32_t* succ_sm, void* pool,
+                      std::int32_t ld, std::int32_t s0, std::int32_t n_sigma, std::int32_t row_begin,
+                      std::int32_t row_end, std::int32_t* out, long long out_row, long long out_col, void* pool,
                       void* stream);
+int launch_transpose_i32(const std::int32_t* in, std::int32_t n, std::int32_t n_sigma, std::int32_t* out, void* stream);
 int launch_chase(std::int32_t n, std::int32_t n_sigma, const std::int32_t* succ_sm, std::int32_t* center_sm,
                  void* stream);
 int launch_labels(std::int32_t n, std::int32_t n_sigma, const std::int32_t* center_sm, std::int32_t* cluster_index_sm,

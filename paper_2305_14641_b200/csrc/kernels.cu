@@ -446,38 +446,47 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
 // (ggd.cpp:7-24). Thread = (row, sigma), sigma fastest: a neighbour's
 // potentials for all sigmas are one contiguous node-major line.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) successors_kernel(int n, const long long* __restrict__ off,
+// Output addressing of the GGD argmin: element (row r of the range, sigma q of
+// the chunk) is written at out[r * out_row + q * out_col] (sigma-major:
+// out_row = 1, out_col = n; node-major row shard: out_row = ld, out_col = 1).
+struct SuccOut {
+    int* out;
+    long long out_row, out_col;
+};
+
+__global__ void __launch_bounds__(kBlock) successors_kernel(const long long* __restrict__ off,
                                                             const int* __restrict__ nbr,
-                                                            const double* __restrict__ v, int S, int s0, int Sc,
-                                                            int* __restrict__ succ_sm) {
+                                                            const double* __restrict__ v, int ld, int s0, int Sc,
+                                                            int row_begin, int rows, SuccOut O) {
     const long long tid = static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x;
-    const int s = s0 + static_cast<int>(tid % Sc);
-    const long long i64 = tid / Sc;
-    if (i64 >= n) return;
-    const int i = static_cast<int>(i64);
+    const int q = static_cast<int>(tid % Sc);
+    const long long r = tid / Sc;
+    if (r >= rows) return;
+    const int s = s0 + q;
+    const int i = row_begin + static_cast<int>(r);
     const long long kend = off[i + 1];
     if (kend - off[i] > kHeavyDegree) return;  // heavy rows: successors_heavy_kernel
     int best = i;
-    double vb = __ldg(v + i64 * S + s);
+    double vb = __ldg(v + static_cast<long long>(i) * ld + s);
     for (long long k = off[i]; k < kend; ++k) {
         const int j = __ldg(nbr + k);
-        const double vj = __ldg(v + static_cast<long long>(j) * S + s);
+        const double vj = __ldg(v + static_cast<long long>(j) * ld + s);
         if (vj < vb || (vj == vb && j < best)) {
             best = j;
             vb = vj;
         }
     }
-    succ_sm[static_cast<long long>(s) * n + i] = best;
+    O.out[r * O.out_row + q * O.out_col] = best;
 }
 
-// Heavy rows (degree > kHeavyDegree, e.g. R-MAT hubs with ~10^5 neighbours):
-// one block per (heavy row, sigma) pair strides over the neighbour list and
-// reduces the lexicographic (v, id) minimum, which is associative, so a hub no
-// longer serialises on one thread. The heavy rows are listed by a marking pass.
-__global__ void mark_heavy_kernel(int n, const long long* __restrict__ off, int* __restrict__ list,
+// Heavy rows (degree > kHeavyDegree, e.g. R-MAT hubs with ~10^5 neighbours)
+// are listed by a marking pass and reduced by one block each: the
+// lexicographic (v, id) minimum is associative, so a hub no longer serialises
+// on one thread.
+__global__ void mark_heavy_kernel(const long long* __restrict__ off, int row_begin, int rows, int* __restrict__ list,
                                   int* __restrict__ count) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n && off[i + 1] - off[i] > kHeavyDegree) list[atomicAdd(count, 1)] = i;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < rows && off[row_begin + r + 1] - off[row_begin + r] > kHeavyDegree) list[atomicAdd(count, 1)] = row_begin + r;
 }
 
 __device__ __forceinline__ bool lex_less(double va, int ia, double vb, int ib) {
@@ -487,9 +496,8 @@ __device__ __forceinline__ bool lex_less(double va, int ia, double vb, int ib) {
 __global__ void __launch_bounds__(kBlock) successors_heavy_kernel(const long long* __restrict__ off,
                                                                   const int* __restrict__ nbr,
                                                                   const double* __restrict__ v, int ld, int s0, int Sc,
-                                                                  int n, const int* __restrict__ list,
-                                                                  const int* __restrict__ count,
-                                                                  int* __restrict__ succ_sm) {
+                                                                  int row_begin, const int* __restrict__ list,
+                                                                  const int* __restrict__ count, SuccOut O) {
     // one block per heavy row: lane = sigma, the 8 warps split the neighbour
     // list (each neighbour's potentials are one coalesced node-major line),
     // then the per-warp minima are combined per sigma in shared memory
@@ -521,9 +529,25 @@ __global__ void __launch_bounds__(kBlock) successors_heavy_kernel(const long lon
                     vb = sv[w][lane];
                     best = si[w][lane];
                 }
-            if (lane < Sc) succ_sm[static_cast<long long>(lane) * n + i] = best;
+            if (lane < Sc) O.out[static_cast<long long>(i - row_begin) * O.out_row + lane * O.out_col] = best;
         }
         __syncthreads();
+    }
+}
+
+// int32 node-major [n][S] -> sigma-major [S][n] (successor shards gathered
+// node-major across ranks are chased sigma-major).
+__global__ void transpose_i32_kernel(const int* __restrict__ in, int n, int S, int* __restrict__ out) {
+    __shared__ int tile[32][33];
+    const int i0 = blockIdx.x * 32, s0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int i = i0 + r, s = s0 + threadIdx.x;
+        if (i < n && s < S) tile[r][threadIdx.x] = in[static_cast<long long>(i) * S + s];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int s = s0 + r, i = i0 + threadIdx.x;
+        if (i < n && s < S) out[static_cast<long long>(s) * n + i] = tile[threadIdx.x][r];
     }
 }
 
@@ -729,38 +753,46 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
 }
 
 int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nbr, const double* v, int ld, int s0,
-                      int n_sigma, std::int32_t* succ_sm, void* pool, void* stream) {
-    // columns s0 .. s0+n_sigma of the node-major V (leading dimension ld) ->
-    // sigma-major succ_sm[n_sigma][n]
+                      int n_sigma, int row_begin, int row_end, std::int32_t* out, long long out_row, long long out_col,
+                      void* pool, void* stream) {
+    (void)n;
     auto st = static_cast<cudaStream_t>(stream);
     auto off = reinterpret_cast<const long long*>(offsets);
+    const int rows = row_end - row_begin;
+    if (rows <= 0) return cudaSuccess;
     void* scratch = nullptr;
-    cudaError_t e = cudaMallocFromPoolAsync(&scratch, sizeof(int) * (static_cast<std::size_t>(n) + 64),
+    cudaError_t e = cudaMallocFromPoolAsync(&scratch, sizeof(int) * (static_cast<std::size_t>(rows) + 64),
                                             static_cast<cudaMemPool_t>(pool), st);
     if (e != cudaSuccess) return e;
     int* count = static_cast<int*>(scratch);
     int* list = count + 32;
     cudaMemsetAsync(count, 0, sizeof(int), st);
-    mark_heavy_kernel<<<grid_for(n), kBlock, 0, st>>>(n, off, list, count);
+    mark_heavy_kernel<<<grid_for(rows), kBlock, 0, st>>>(off, row_begin, rows, list, count);
     count_launch(2);
-    // thread = (row, sigma), sigma fastest: a neighbour's potentials for the
-    // chunk's sigmas are one contiguous node-major line
     static int num_sms = 0;
     if (!num_sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
+    // thread = (row, sigma), sigma fastest: a neighbour's potentials for the
+    // chunk's sigmas are one contiguous node-major line
     for (int c0 = 0; c0 < n_sigma; c0 += 32) {
         const int Sc = std::min(32, n_sigma - c0);
-        const long long threads = static_cast<long long>(n) * Sc;
-        successors_kernel<<<grid_for(threads), kBlock, 0, st>>>(
-            n, off, nbr, v, ld, s0 + c0, Sc, succ_sm - static_cast<long long>(s0) * n);
-        successors_heavy_kernel<<<num_sms * 8, kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, n, list, count,
-                                                               succ_sm + static_cast<long long>(c0) * n);
+        const SuccOut O{out + c0 * out_col, out_row, out_col};
+        const long long threads = static_cast<long long>(rows) * Sc;
+        successors_kernel<<<grid_for(threads), kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, rows, O);
+        successors_heavy_kernel<<<num_sms * 8, kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, list, count, O);
         count_launch(2);
     }
     cudaFreeAsync(scratch, st);
+    return cudaGetLastError();
+}
+
+int launch_transpose_i32(const std::int32_t* in, int n, int n_sigma, std::int32_t* out, void* stream) {
+    const dim3 grid((n + 31) / 32, (n_sigma + 31) / 32);
+    transpose_i32_kernel<<<grid, dim3(32, 8), 0, static_cast<cudaStream_t>(stream)>>>(in, n, n_sigma, out);
+    count_launch();
     return cudaGetLastError();
 }
 

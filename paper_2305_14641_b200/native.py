@@ -79,12 +79,16 @@ def _load():
         "gqc_dev_potentials": [P, P, i32, i32, i32, P, P],
         "gqc_dev_ggd": [P, P, i32, P, P, P, P, P, C.c_size_t, P],
         "gqc_dev_transpose": [P, i32, i32, P, P],
+        "gqc_dev_successors": [P, P, i32, i32, i32, P, P],
+        "gqc_dev_resolve": [i32, i32, P, P, P, P, P, C.c_size_t, P],
     }.items():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = C.c_int
     lib.gqc_dev_ggd_workspace.argtypes = [i32, i32]
     lib.gqc_dev_ggd_workspace.restype = C.c_size_t
+    lib.gqc_dev_resolve_workspace.argtypes = [i32, i32]
+    lib.gqc_dev_resolve_workspace.restype = C.c_size_t
     return lib
 
 
@@ -308,3 +312,25 @@ def dev_ggd(dg: DeviceCsr, v, n_sigma: int, succ, center, cluster_index, num_clu
 def dev_transpose(v_nm, n: int, n_sigma: int, v_sm, stream=None):
     sp = None if stream is None else C.c_void_p(stream.cuda_stream)
     _check(_lib.gqc_dev_transpose(C.c_void_p(v_nm.data_ptr()), n, n_sigma, C.c_void_p(v_sm.data_ptr()), sp))
+
+
+def dev_successors(dg: DeviceCsr, v, n_sigma: int, row_begin: int, row_end: int, succ_rows, stream=None):
+    """GGD argmin of rows [row_begin, row_end) from the full node-major V,
+    node-major into succ_rows[(i - row_begin), k] (int32 device tensor)."""
+    cs = dg.c_struct()
+    sp = None if stream is None else C.c_void_p(stream.cuda_stream)
+    _check(_lib.gqc_dev_successors(C.byref(cs), C.c_void_p(v.data_ptr()), int(n_sigma), int(row_begin), int(row_end),
+                                   C.c_void_p(succ_rows.data_ptr()), sp))
+
+
+def dev_resolve_workspace(n: int, n_sigma: int) -> int:
+    return int(_lib.gqc_dev_resolve_workspace(n, n_sigma))
+
+
+def dev_resolve(n: int, n_sigma: int, succ_nm, center, cluster_index, num_clusters, workspace, stream=None):
+    """Centers / dense cluster indices (sigma-major) and counts from a
+    node-major successor matrix [n, n_sigma]."""
+    sp = None if stream is None else C.c_void_p(stream.cuda_stream)
+    p = lambda t: C.c_void_p(t.data_ptr())
+    _check(_lib.gqc_dev_resolve(int(n), int(n_sigma), p(succ_nm), p(center), p(cluster_index), p(num_clusters),
+                                p(workspace), workspace.numel() * workspace.element_size(), sp))

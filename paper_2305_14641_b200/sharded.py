@@ -56,3 +56,47 @@ def sharded_field(n: int, n_sigma: int, compute_rows: Callable[[int, int, torch.
     if end > begin:
         compute_rows(begin, end, shard[: end - begin])
     return gather_rows(shard, n, group, full_buf)
+
+
+class ShardedSweep:
+    """One multi-GPU step of the sweep with the GGD argmin sharded too:
+
+        potentials of own rows -> all-gather V (fp64) ->
+        successors of own rows -> all-gather succ (int32) -> centers/labels
+
+    Every collective is an equal-slab all-gather of node-major rows. The
+    device operations are injected (native gqc_dev_* on the GPU; the oracle in
+    the CPU gloo tests), so this class is the whole host-side schedule.
+
+      potentials_rows(begin, end, out[rows, S])
+      successors_rows(V[n, S], begin, end, out[rows, S] int32)
+      resolve(succ[n, S] int32) -> (center [S, n], cluster_index [S, n], num_clusters [S])
+    """
+
+    def __init__(self, n, n_sigma, rank, world, device, potentials_rows, successors_rows, resolve, group=None):
+        self.n, self.S, self.rank, self.world, self.group = n, n_sigma, rank, world, group
+        self.block = row_block(n, world)
+        self.begin, self.end = row_shard(n, world, rank)
+        self.potentials_rows, self.successors_rows, self.resolve = potentials_rows, successors_rows, resolve
+        self.shard_v = torch.zeros((self.block, n_sigma), dtype=torch.float64, device=device)
+        self.shard_s = torch.zeros((self.block, n_sigma), dtype=torch.int32, device=device)
+        big = world > 1
+        self.full_v = torch.empty((world * self.block, n_sigma), dtype=torch.float64, device=device) if big else None
+        self.full_s = torch.empty((world * self.block, n_sigma), dtype=torch.int32, device=device) if big else None
+
+    def potentials(self):
+        rows = self.end - self.begin
+        if rows > 0:
+            self.potentials_rows(self.begin, self.end, self.shard_v[:rows])
+        return gather_rows(self.shard_v, self.n, self.group, self.full_v)
+
+    def successors(self, V):
+        rows = self.end - self.begin
+        if rows > 0:
+            self.successors_rows(V, self.begin, self.end, self.shard_s[:rows])
+        return gather_rows(self.shard_s, self.n, self.group, self.full_s)
+
+    def step(self):
+        V = self.potentials()
+        succ = self.successors(V)
+        return V, succ, self.resolve(succ)

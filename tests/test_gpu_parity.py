@@ -342,3 +342,32 @@ def test_hub_rows_heavy_argmin_and_scheduling():
     for s in (1.0, 5.0):
         vo = O.potentials(g.offsets, g.nbr, g.wt, 10.0, s, workers=8)
         assert np.array_equal(N.build_successors(g.csr(N), vo), O.build_successors(g.offsets, g.nbr, vo))
+
+
+def test_row_sharded_successors_and_resolve_match_full_ggd():
+    # the multi-GPU schedule's device pieces: successors of row shards
+    # (node-major) assemble to the full argmin, and resolve() reproduces
+    # dev_ggd's centers / labels / counts
+    import torch
+    from paper_2305_14641_b200 import sharded
+    g = H.random_graph(5003, 8.0, seed=31, unit=True)
+    csr = g.csr(N)
+    sig = O.log_sigma_grid(10.0, 32)
+    S = len(sig)
+    v_ref, s_ref, c_ref, ci_ref, nc_ref = _dev_labels(csr, sig)
+    dg = N.DeviceCsr(csr)
+    center = torch.empty((S, g.n), dtype=torch.int32, device="cuda")
+    ci, nc = torch.empty_like(center), torch.empty(S, dtype=torch.int32, device="cuda")
+    ws = torch.empty(N.dev_resolve_workspace(g.n, S), dtype=torch.uint8, device="cuda")
+    for world in (1, 3):
+        V = torch.empty((g.n, S), dtype=torch.float64, device="cuda")
+        N.dev_potentials(dg, sig, 0, g.n, V)
+        succ = torch.empty((g.n, S), dtype=torch.int32, device="cuda")
+        for r in range(world):
+            b, e = sharded.row_shard(g.n, world, r)
+            N.dev_successors(dg, V, S, b, e, succ[b:e])
+        N.dev_resolve(g.n, S, succ, center, ci, nc, ws)
+        torch.cuda.synchronize()
+        assert np.array_equal(succ.cpu().numpy().T, s_ref)
+        assert np.array_equal(center.cpu().numpy(), c_ref) and np.array_equal(ci.cpu().numpy(), ci_ref)
+        assert nc.cpu().tolist() == nc_ref.tolist()

@@ -63,3 +63,52 @@ def test_gloo_sharded_field_matches_single_process(world, tmp_path):
     mp.start_processes(_worker, args=(world, _free_port(), str(result)), nprocs=world, join=True,
                        start_method="spawn")
     assert result.read_text() == "ok"
+
+
+def _worker_ggd(rank, world, port, result_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import pyoracle as O
+        from tests import helpers as H
+        g = H.random_graph(97, 3.0, seed=12, unit=True)
+        sig = [0.7, 2.3, 5.0, 30.0]
+
+        def potentials_rows(begin, end, out):
+            rows = np.arange(begin, end, dtype=np.int32)
+            for q, s in enumerate(sig):
+                out[:, q] = torch.from_numpy(O.potentials_rows(g.offsets, g.nbr, g.wt, 10.0, s, rows))
+
+        def successors_rows(V, begin, end, out):
+            for q in range(len(sig)):
+                full = O.build_successors(g.offsets, g.nbr, V[:, q].numpy().copy())
+                out[:, q] = torch.from_numpy(full[begin:end])
+
+        def resolve(succ):
+            res = [O.resolve_centers(succ[:, q].numpy().copy()) for q in range(len(sig))]
+            return res
+
+        sweep = sharded.ShardedSweep(g.n, len(sig), rank, world, "cpu", potentials_rows, successors_rows, resolve)
+        V, succ, res = sweep.step()
+        ok = True
+        for q, s in enumerate(sig):
+            v, so, co, cio, ko = O.cluster(g.offsets, g.nbr, g.wt, 10.0, s)
+            ok &= np.array_equal(V[:, q].numpy().view(np.int64), v.view(np.int64))
+            ok &= np.array_equal(succ[:, q].numpy(), so)
+            ok &= np.array_equal(res[q][0], co) and np.array_equal(res[q][1], cio) and res[q][2] == ko
+        with open(f"{result_path}.{rank}", "w") as f:
+            f.write("ok" if ok else "mismatch")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_sharded_ggd_matches_single_process(world, tmp_path):
+    # the multi-GPU schedule with the GGD argmin sharded: every rank ends with
+    # the single-process labels
+    result = tmp_path / "r"
+    mp.start_processes(_worker_ggd, args=(world, _free_port(), str(result)), nprocs=world, join=True,
+                       start_method="spawn")
+    for r in range(world):
+        assert (tmp_path / f"r.{r}").read_text() == "ok"
