@@ -72,8 +72,6 @@ def _declare(L):
     L.orc_detect_mutation.argtypes = [i32, P, P, P, P, P, P]
     L.orc_scores.argtypes = [i64, P, i32, P, i32, P]
     L.orc_modularity.argtypes = [i32, P, P, P, P, f64, P]
-    for name in dir(L):
-        pass
 
 
 def _check(status):

@@ -137,12 +137,6 @@ bool all_unit(const double* w, long long nnz) {
     return true;
 }
 
-// Weight information the potential launches need from the host side.
-struct HostWeights {
-    const double* w = nullptr;  // host weights (nnz) or nullptr
-    std::vector<double> last_row_w;
-};
-
 // glibc exp over a [count][S] block, split across host threads.
 void host_exp_table(const double* d2, long long count, const std::vector<double>& neg_inv, int S, double* out) {
     const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
@@ -219,7 +213,6 @@ void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S,
         P.offsets = g.offsets;
         P.nbr = g.nbr;
         P.w = g.w;
-        P.w2 = g.W * g.W;
         P.tail = tail ? 1 : 0;
         P.out = v_nm;
         P.out_ld = S;

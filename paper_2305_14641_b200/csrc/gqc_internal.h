@@ -38,7 +38,6 @@ struct PotentialLaunch {
     const std::int64_t* offsets;
     const std::int32_t* nbr;
     const double* w;           // nullptr for unit weights
-    double w2;                 // W*W
     int tail;                  // column n-1 uses the glibc tail constants
     int weight_mode;
     const double* entry_exp;   // kEntryTable: [nnz][entry_ld] at column entry_col0 + s
