@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -64,6 +66,38 @@ gqc_status guarded(F&& f) {
     }
 }
 
+// Opt-in stage tracing (GQC_TRACE=1): CUDA events on the compute stream
+// around each stage of a host-API call, printed to stderr when it returns.
+struct Tracer {
+    bool on = false;
+    cudaStream_t st = nullptr;
+    std::vector<std::pair<std::string, cudaEvent_t>> marks;
+    explicit Tracer(cudaStream_t s) : st(s) {
+        const char* e = std::getenv("GQC_TRACE");
+        on = e && *e && *e != '0';
+        mark("begin");
+    }
+    void mark(const char* what) {
+        if (!on) return;
+        cudaEvent_t ev;
+        cudaEventCreate(&ev);
+        cudaEventRecord(ev, st);
+        marks.emplace_back(what, ev);
+    }
+    ~Tracer() {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        std::string line = "[gqc trace]";
+        for (std::size_t k = 1; k < marks.size(); ++k) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, marks[k - 1].second, marks[k].second);
+            line += " " + marks[k].first + "=" + std::to_string(ms) + "ms";
+        }
+        for (auto& m : marks) cudaEventDestroy(m.second);
+        std::fprintf(stderr, "%s\n", line.c_str());
+    }
+};
+
 // Grow-only device buffers, one set per device: repeated calls reuse memory.
 struct DevBuf {
     void* p = nullptr;
@@ -85,7 +119,9 @@ struct DevBuf {
 struct DeviceCtx {
     cudaStream_t stream = nullptr;
     cudaStream_t copy = nullptr;   // host<->device copies overlapped with compute
+    cudaStream_t slab[4] = {};     // concurrent per-slab potential launches
     cudaEvent_t ev[16] = {};
+    cudaEvent_t slab_done[4] = {};
     cudaMemPool_t pool = nullptr;  // stream-ordered scratch that keeps its memory
     DevBuf off, nbr, w, v_nm, v_sm, succ, center, ci, nc, ws, tail, entry;
 };
@@ -103,7 +139,9 @@ DeviceCtx& ctx() {
     if (!c.stream) {
         cuda_check(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking), "cudaStreamCreate");
         cuda_check(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking), "cudaStreamCreate");
+        for (auto& sl : c.slab) cuda_check(cudaStreamCreateWithFlags(&sl, cudaStreamNonBlocking), "cudaStreamCreate");
         for (auto& e : c.ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        for (auto& e : c.slab_done) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     }
     if (!c.pool) {
         cudaMemPoolProps props{};
@@ -210,6 +248,7 @@ void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S,
         P.n_sigma = Sc;
         P.row_begin = row_begin;
         P.row_end = row_end;
+        P.nnz = g.nnz;
         P.offsets = g.offsets;
         P.nbr = g.nbr;
         P.w = g.w;
@@ -417,6 +456,7 @@ gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_s
         if (g->offsets[0] != 0 || g->offsets[g->n] != g->nnz) fail(GQC_EINVAL, "CSR offsets do not match nnz");
         DeviceCtx& C = ctx();
         cudaStream_t st = C.stream, cs = C.copy;
+        Tracer tr(st);
         const int n = g->n;
         const long long nnz = g->nnz;
         const bool weighted = g->w && !all_unit(g->w, nnz);
@@ -460,12 +500,18 @@ gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_s
                     cuda_check(cudaMemcpyAsync(w + a, g->w + a, (b - a) * sizeof(double), cudaMemcpyHostToDevice, cs),
                                "copy weights");
             }
+            // each slab's potentials on its own stream: slabs run concurrently
+            // (a slab holding a hub row does not hold back the others)
             cuda_check(cudaEventRecord(C.ev[k], cs), "event");
-            cuda_check(cudaStreamWaitEvent(st, C.ev[k], 0), "wait");
+            cudaStream_t ss = C.slab[k];
+            cuda_check(cudaStreamWaitEvent(ss, C.ev[k], 0), "wait");
             if (bound[k + 1] > bound[k])
                 run_potentials(C, d, sigmas, n_sigma, bound[k], bound[k + 1], v_nm + static_cast<std::size_t>(bound[k]) * n_sigma,
-                               weighted ? g->w : nullptr, st, g->offsets);
+                               weighted ? g->w : nullptr, ss, g->offsets);
+            cuda_check(cudaEventRecord(C.slab_done[k], ss), "event");
         }
+        for (int k = 0; k < slabs; ++k) cuda_check(cudaStreamWaitEvent(st, C.slab_done[k], 0), "wait");
+        tr.mark("potentials");
         if (v_out) {  // sigma-major copy of the field
             double* src = v_nm;
             if (n_sigma > 1) {
@@ -490,6 +536,7 @@ gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_s
             cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, s0, Sc, 0, n, ds + o, 1, n, C.pool, st), "successor kernel");
             cuda_check(launch_chase(n, Sc, ds + o, dc + o, st), "chase kernel");
             cuda_check(launch_labels(n, Sc, dc + o, dci + o, dnc + s0, ws, wsb, st), "label kernels");
+            tr.mark("ggd_chunk");
             cudaEvent_t e = C.ev[ev_i];
             ev_i = ev_i == 15 ? 9 : ev_i + 1;
             cuda_check(cudaEventRecord(e, st), "event");
@@ -503,6 +550,9 @@ gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_s
             cuda_check(cudaMemcpyAsync(num_clusters_out + s0, dnc + s0, Sc * sizeof(int), cudaMemcpyDeviceToHost, cs),
                        "copy counts");
         }
+        cuda_check(cudaEventRecord(C.ev[8], cs), "event");
+        cuda_check(cudaStreamWaitEvent(st, C.ev[8], 0), "wait");
+        tr.mark("downloads");
         cuda_check(cudaStreamSynchronize(cs), "cluster sweep (copies)");
         cuda_check(cudaStreamSynchronize(st), "cluster sweep");
     });

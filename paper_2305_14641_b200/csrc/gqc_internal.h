@@ -35,6 +35,7 @@ struct PotentialLaunch {
     std::int32_t n;
     std::int32_t n_sigma;      // sigmas in this launch (<= kMaxSigmaPerLaunch)
     std::int32_t row_begin, row_end;
+    std::int64_t nnz;          // entries of the whole CSR (hub threshold)
     const std::int64_t* offsets;
     const std::int32_t* nbr;
     const double* w;           // nullptr for unit weights

@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
+#include <utility>
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -111,8 +113,27 @@ struct PrefixTable {
 // no warp idles while another still owns a backlog.
 struct RowSched {
     const int* order;  // row ids, heaviest first
-    int* counter;      // next position in `order` (zeroed per launch)
+    int* counter;      // next position in `order`
+    const int* limit;  // rows to take (device), or nullptr for the whole range
 };
+
+// Hub rows: a row so long that, walked by one warp sharing its scheduler with
+// seven others, it would outlast the rest of the sweep (R-MAT's hub has ~10^5
+// neighbours) gets an SM to itself: a companion launch on a side stream runs
+// one warp per block with enough dynamic shared memory that no other block
+// fits on that SM. The main launch skips those rows.
+constexpr int kMaxHubs = 16;
+constexpr int kHubSmemBytes = 196 * 1024;
+
+__global__ void hub_split_kernel(const int* __restrict__ deg_sorted, int rows, long long threshold,
+                                 int* __restrict__ hub_count, int* __restrict__ main_counter,
+                                 int* __restrict__ hub_counter) {
+    int h = 0;
+    while (h < kMaxHubs && h < rows && deg_sorted[h] > threshold) ++h;
+    *hub_count = h;
+    *main_counter = h;
+    *hub_counter = 0;
+}
 constexpr int kRowsPerGrab = 2;
 constexpr int kHeavyDegree = 128;  // GGD argmin: rows above this degree use a block each
 
@@ -354,15 +375,16 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
         }
     };
 
-    const int nrows = P.row_end - P.row_begin;
+    const int nrows = R.limit ? *R.limit : P.row_end - P.row_begin;
     int grab = 0, left = 0;
     for (;;) {
         if (left == 0) {  // next batch of rows, heaviest first
+            const int take = R.limit ? 1 : kRowsPerGrab;  // hub rows: one per warp
             int g0 = 0;
-            if (lane == 0) g0 = atomicAdd(R.counter, kRowsPerGrab);
+            if (lane == 0) g0 = atomicAdd(R.counter, take);
             grab = __shfl_sync(kFull, g0, 0);
             if (grab >= nrows) break;
-            left = min(kRowsPerGrab, nrows - grab);
+            left = min(take, nrows - grab);
         }
         const int i = R.order[grab];
         ++grab;
@@ -651,6 +673,25 @@ __global__ void resolve_error_kernel(int n, const int* __restrict__ term, unsign
 
 int grid_for(long long threads) { return static_cast<int>((threads + kBlock - 1) / kBlock); }
 
+// Side stream and fork/join events for companion launches, one set per parent
+// stream (calls into libgqc are serialized, so the map needs no lock of its own).
+struct SideStream {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream& side_for(cudaStream_t parent) {
+    static std::map<std::pair<int, cudaStream_t>, SideStream> all;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    SideStream& c = all[{dev, parent}];
+    if (!c.stream) {
+        cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming);
+    }
+    return c;
+}
+
 }  // namespace
 
 int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* stream) {
@@ -710,25 +751,42 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
         e = cub::DeviceRadixSort::SortPairsDescending(temp, sort_bytes, deg_in, deg_out, id_in, id_out, rows, 0, 32, st);
         count_launch(2);
         if (e != cudaSuccess) return e;
-        cudaMemsetAsync(counter, 0, sizeof(int), st);
-        const RowSched R{id_out, counter};
+        // hub rows (see hub_split_kernel): longer than ~1/4096 of the entries
+        int* hub_count = counter + 1;
+        int* hub_counter = counter + 2;
+        const long long threshold = std::max<long long>(4096, p.nnz / 4096);
+        hub_split_kernel<<<1, 1, 0, st>>>(deg_out, rows, threshold, hub_count, counter, hub_counter);
+        count_launch();
+        const RowSched R{id_out, counter, nullptr};
+        const RowSched Rh{id_out, hub_counter, hub_count};
         const long long want = (static_cast<long long>(rows) + kBlock / 32 - 1) / (kBlock / 32);
         const dim3 wgrid(static_cast<unsigned>(
             std::min<long long>(want, static_cast<long long>(num_sms) * kWarpKernelBlocksPerSM)));
+        SideStream& side = side_for(st);
+        cudaEventRecord(side.fork, st);
+        cudaStreamWaitEvent(side.stream, side.fork, 0);
+        auto launch = [&](auto kernel) {
+            cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHubSmemBytes);
+            kernel<<<kMaxHubs, 32, kHubSmemBytes, side.stream>>>(p, T, Rh);  // first: hub blocks claim SMs
+            kernel<<<wgrid, kBlock, 0, st>>>(p, T, R);
+            count_launch(2);
+        };
         switch (p.weight_mode) {
             case kUnit:
-                if (ff) potential_warp_kernel<true, kUnit><<<wgrid, kBlock, 0, st>>>(p, T, R);
-                else potential_warp_kernel<false, kUnit><<<wgrid, kBlock, 0, st>>>(p, T, R);
+                if (ff) launch(potential_warp_kernel<true, kUnit>);
+                else launch(potential_warp_kernel<false, kUnit>);
                 break;
             case kDevicePexp:
-                if (ff) potential_warp_kernel<true, kDevicePexp><<<wgrid, kBlock, 0, st>>>(p, T, R);
-                else potential_warp_kernel<false, kDevicePexp><<<wgrid, kBlock, 0, st>>>(p, T, R);
+                if (ff) launch(potential_warp_kernel<true, kDevicePexp>);
+                else launch(potential_warp_kernel<false, kDevicePexp>);
                 break;
             default:
-                if (ff) potential_warp_kernel<true, kEntryTable><<<wgrid, kBlock, 0, st>>>(p, T, R);
-                else potential_warp_kernel<false, kEntryTable><<<wgrid, kBlock, 0, st>>>(p, T, R);
+                if (ff) launch(potential_warp_kernel<true, kEntryTable>);
+                else launch(potential_warp_kernel<false, kEntryTable>);
                 break;
         }
+        cudaEventRecord(side.join, side.stream);
+        cudaStreamWaitEvent(st, side.join, 0);
         cudaFreeAsync(sched, st);
     } else {
         switch (p.weight_mode) {

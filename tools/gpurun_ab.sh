@@ -10,9 +10,11 @@ python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 run A
 for v in "$@"; do
   cp paper_2305_14641_b200/csrc/kernels.cu /tmp/k.bak
-  sed -i "$v" paper_2305_14641_b200/csrc/kernels.cu
+  cp paper_2305_14641_b200/csrc/ff_chain.cuh /tmp/f.bak
+  sed -i "$v" paper_2305_14641_b200/csrc/kernels.cu paper_2305_14641_b200/csrc/ff_chain.cuh
   make -s > /dev/null 2>&1
   run "$v"
   cp /tmp/k.bak paper_2305_14641_b200/csrc/kernels.cu
+  cp /tmp/f.bak paper_2305_14641_b200/csrc/ff_chain.cuh
 done
 make -s > /dev/null 2>&1
