@@ -64,9 +64,13 @@ Csr build_csr(std::int32_t n, const std::vector<std::pair<std::int32_t, std::int
 
 // Planted partition: `blocks` blocks of `size` consecutive ids; round(n*deg/2)
 // edge draws, a fraction `intra` inside a uniformly chosen block.
+thread_local std::vector<std::int32_t> g_labels;  // planted communities of the last graph
+
 Csr sbm(std::int32_t blocks, std::int32_t size, double avg_deg, double intra, std::uint64_t seed) {
     Rng r(seed);
     const std::int32_t n = blocks * size;
+    g_labels.resize(n);
+    for (std::int32_t i = 0; i < n; ++i) g_labels[i] = i / size;
     const std::int64_t m = std::llround(n * avg_deg / 2.0);
     std::vector<std::pair<std::int32_t, std::int32_t>> e;
     e.reserve(m);
@@ -129,7 +133,11 @@ Csr lfr(std::int32_t n, double avg_deg, double tau1, double kmax, double tau2, d
     std::vector<std::int32_t> ext_stubs;
     std::int64_t base = 0;
     std::vector<std::int32_t> stubs;
+    g_labels.assign(n, 0);
+    std::int32_t community = 0;
     for (std::int32_t sz : sizes) {
+        for (std::int32_t t = 0; t < sz; ++t) g_labels[perm[base + t]] = community;
+        ++community;
         stubs.clear();
         for (std::int32_t t = 0; t < sz; ++t) {
             const std::int32_t node = perm[base + t];
@@ -152,6 +160,7 @@ Csr lfr(std::int32_t n, double avg_deg, double tau1, double kmax, double tau2, d
 Csr rmat(int scale, double edge_factor, double a, double b, double c, std::uint64_t seed) {
     Rng r(seed);
     const std::int32_t n = 1 << scale;
+    g_labels.clear();  // no planted partition
     const std::int64_t m = static_cast<std::int64_t>(edge_factor * n);
     std::vector<std::pair<std::int32_t, std::int32_t>> e;
     e.reserve(m);
@@ -234,6 +243,14 @@ std::int64_t gg_random_edges(std::int32_t n, double avg_deg, int unit, std::uint
         m = 1;
     }
     return m;
+}
+
+// Planted community of every node of the last sbm/lfr graph (n entries);
+// returns 0 when the last generator has none.
+int gg_labels(std::int32_t* out) {
+    if (g_labels.empty()) return 0;
+    std::memcpy(out, g_labels.data(), g_labels.size() * sizeof(std::int32_t));
+    return 1;
 }
 
 int gg_copy(std::int64_t* offsets, std::int32_t* nbr) {

@@ -41,6 +41,7 @@ def lib():
         L.gg_random_edges.argtypes = [C.c_int32, C.c_double, C.c_int, C.c_uint64, P, P, P, C.c_int64]
         L.gg_random_edges.restype = C.c_int64
         L.gg_copy.argtypes = [P, P]
+        L.gg_labels.argtypes = [P]
         _lib = L
     return _lib
 
@@ -86,6 +87,25 @@ def random_edges(n, avg_deg, unit=False, seed=1):
     m = lib().gg_random_edges(n, avg_deg, 1 if unit else 0, seed, u.ctypes.data_as(C.c_void_p),
                               v.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p), cap)
     return u[:m].copy(), v[:m].copy(), w[:m].copy()
+
+
+def labels(n):
+    """Planted communities of the last sbm()/lfr() graph (int32[n]); call it
+    after that generator and before the next one. None for R-MAT."""
+    out = np.empty(n, np.int32)
+    return out if lib().gg_labels(out.ctypes.data_as(C.c_void_p)) else None
+
+
+def write_edge_list(path, offsets, nbr):
+    """`u v` per undirected edge (u < v) in CSR order."""
+    n = len(offsets) - 1
+    rows = np.repeat(np.arange(n, dtype=np.int32), np.diff(offsets))
+    keep = rows < nbr
+    uv = np.stack([rows[keep], nbr[keep]], axis=1)
+    with open(path, "w") as f:
+        for a in range(0, len(uv), 1 << 20):
+            f.write("\n".join(f"{u} {v}" for u, v in uv[a:a + (1 << 20)].tolist()))
+            f.write("\n")
 
 
 sbm_100k = sbm

@@ -196,10 +196,19 @@ GQC_HD inline void ff_pass(Chain& ch, const double c, int& L) {
         return;
     }
     const double m = ok ? max_steps(ch, room_of(ch)) : 0.0;
+    const double top = ch.top;
     ch.s = gqc_add(gqc_fma(m, ch.inc, ch.s), c);
     L -= static_cast<int>(m) + 1;
+    if (ok) {
+        // a settled crossing lands in the next binade [top, 2 top): the exact
+        // sum is below top + c and c < base/2 = top/4; c stays jumpable there
+        ch.top = gqc_add(top, top);
+        ch.inc = gqc_sub(gqc_add(top, c), top);
+        ch.flags = kJump | (exp_field(top) == ch.f_tie ? kTie : 0);
+    } else {
+        refresh(ch, c);  // a single real add (c >= base/2, or an odd tie)
+    }
     if (L <= 0) return;
-    refresh(ch, c);  // idempotent when the real add stayed in the binade
     const double t2 = gqc_fma(static_cast<double>(L), ch.inc, ch.s);
     if (settled(ch) && t2 < ch.top) {
         ch.s = t2;

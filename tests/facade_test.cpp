@@ -126,6 +126,20 @@ int main(int argc, char** argv) {
         std::istringstream repeat("a x\na x\nb y\nc x\n");
         CHECK(parse_labels(repeat, g, "<test>").num_classes() == 2);
     }
+    // integer names (value -> id array instead of a hash map): ids follow first
+    // appearance, and only the canonical spelling of a name is that name
+    {
+        Graph g = from_text("7 3\n3 100\n0 7\n");
+        CHECK(g.num_nodes() == 4 && g.id_of("7") == 0 && g.id_of("3") == 1 && g.id_of("100") == 2 && g.id_of("0") == 3);
+        CHECK(g.id_of("07") == -1 && g.id_of("+7") == -1 && g.id_of("5") == -1 && g.id_of("101") == -1 &&
+              g.id_of("99999999999") == -1 && g.id_of("") == -1 && g.id_of("a") == -1);
+        std::istringstream ok("0 p\n3 q\n7 p\n100 q\n");
+        CHECK(parse_labels(ok, g, "<test>").label_of(g.id_of("100")) == 1);
+        std::istringstream padded("0 p\n3 q\n07 p\n100 q\n");
+        CHECK_THROWS(parse_labels(padded, g, "<test>"), IoError);
+        Graph mixed = from_text("7 3\n07 x\n");  // "07" is its own node next to "7"
+        CHECK(mixed.num_nodes() == 4 && mixed.id_of("07") == 2 && mixed.id_of("7") == 0);
+    }
     // karate fixture shape (graph_test.cpp:165-178)
     {
         Graph g = load_edge_list(data + "/karate.edges", 10.0);
