@@ -251,51 +251,44 @@ def run_native(args):
     begin, end = sharded.row_shard(n, world, rank)
     rows = end - begin
 
+    chunk = sharded.sigma_chunk(S, world)
     with torch.cuda.stream(stream):
-        center = torch.empty((S, n), dtype=torch.int32, device=dev)
-        ci = torch.empty_like(center)
-        nc = torch.empty(S, dtype=torch.int32, device=dev)
-        ws = torch.empty(N.dev_resolve_workspace(n, S), dtype=torch.uint8, device=dev)
+        center = torch.empty((chunk, n), dtype=torch.int32, device=dev)
+        ws = torch.empty(N.dev_ggd_workspace(n, chunk), dtype=torch.uint8, device=dev)
         flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 512 MiB > 126 MB L2
     torch.cuda.synchronize(dev)
 
     launches = [0]
     ev = {}
 
-    def pot_rows(b, e, out):
-        N.dev_potentials(dg, sig, b, e, out, stream)
+    def pot_packed(b, e, send, ch, stride):
+        N.dev_potentials_packed(dg, sig, b, e, send, ch, stride, stream)
         launches[0] += N.last_launch_count()
 
-    def succ_rows(V, b, e, out):
-        N.dev_successors(dg, V, S, b, e, out, stream)
-        launches[0] += N.last_launch_count()
-
-    def resolve(succ):
-        N.dev_resolve(n, S, succ, center, ci, nc, ws, stream)
+    def ggd(v_chunk, ci_out, nc_out):
+        N.dev_ggd(dg, v_chunk, chunk, None, center, ci_out, nc_out, ws, stream)
         launches[0] += N.last_launch_count()
 
     with torch.cuda.stream(stream):
-        sweep = sharded.ShardedSweep(n, S, rank, world, dev, pot_rows, succ_rows, resolve)
-    shard = sweep.shard_v
+        sweep = sharded.SigmaShardedSweep(n, S, rank, world, dev, pot_packed, ggd)
+    shard = sweep.send  # this rank's rows, packed by sigma chunk
 
     def step(record=False):
-        # potentials of own rows -> all-gather V -> GGD argmin of own rows ->
-        # all-gather succ -> centers / labels (sharded.ShardedSweep)
+        # potentials of own rows (all sigmas) -> all-to-all V by sigma chunk ->
+        # GGD of own sigma chunk -> all-gather labels (sharded.SigmaShardedSweep)
         with torch.cuda.stream(stream):
             if record:
                 ev["p0"].record(stream)
-            if rows > 0:
-                pot_rows(begin, end, sweep.shard_v[:rows])
+            sweep.potentials()
             if record:
                 ev["p1"].record(stream)
-            V = sharded.gather_rows(sweep.shard_v, n, None, sweep.full_v)
+            v = sweep.exchange()
             if record:
                 ev["p2"].record(stream)
-            succ = sweep.successors(V)
+            sweep.ggd(v)
             if record:
                 ev["p3"].record(stream)
-            sweep.resolve(succ)
-        return V
+            sweep.gather()
 
     sampler = ClockSampler(local)
     sampler.start()
@@ -303,7 +296,7 @@ def run_native(args):
         step()
     torch.cuda.synchronize(dev)
 
-    per_step, parts = [], {"potentials": [], "allgather_v": [], "successors_allgather_succ": [], "resolve": []}
+    per_step, parts = [], {"potentials": [], "alltoall_v": [], "ggd": [], "allgather_labels": []}
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -323,9 +316,9 @@ def run_native(args):
         e1.synchronize()
         per_step.append(e0.elapsed_time(e1))
         parts["potentials"].append(ev["p0"].elapsed_time(ev["p1"]))
-        parts["allgather_v"].append(ev["p1"].elapsed_time(ev["p2"]))
-        parts["successors_allgather_succ"].append(ev["p2"].elapsed_time(ev["p3"]))
-        parts["resolve"].append(ev["p3"].elapsed_time(e1))
+        parts["alltoall_v"].append(ev["p1"].elapsed_time(ev["p2"]))
+        parts["ggd"].append(ev["p2"].elapsed_time(ev["p3"]))
+        parts["allgather_labels"].append(ev["p3"].elapsed_time(e1))
     torch.cuda.synchronize(dev)
     wall = time.perf_counter() - t_wall
     sampler.mark(t_epoch0, time.time())
@@ -362,7 +355,7 @@ def run_native(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         threads = os.cpu_count() or 1
         pps, srows, el, vref = cpu_sample(off, nbr, sig, args.cpu_seconds, threads)
-        V_host_rows = shard[torch.from_numpy(srows.astype(np.int64)).to(dev)].cpu().numpy()
+        V_host_rows = shard.view(-1, S)[torch.from_numpy(srows.astype(np.int64)).to(dev)].cpu().numpy()
         same = bool(np.array_equal(V_host_rows.view(np.int64), vref.view(np.int64)))
         cpu = {"value": pps / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"{len(srows)} strided rows x {S} sigmas ({len(srows) * n * S:.3e} pairs) in {el:.1f}s, "
@@ -375,9 +368,11 @@ def run_native(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "n_nodes": n, "nnz": int(nnz), "n_sigma": S,
                        "sigma_grid": f"log_sigma_grid(10, {S})", "kernel": args.kernel,
-                       "parallelism": f"row-shard x{world} + all-gather(V)",
+                       "parallelism": f"potentials row-shard x{world}; all-to-all(V) by sigma chunk; "
+                                      f"GGD sigma-shard x{world}; all-gather(labels)",
                        "l2": "512 MiB write between timed steps (excluded from the per-step events)",
-                       "step": "potentials(all rows, all sigmas) + all-gather V + GGD(succ, centers, labels)"},
+                       "step": "potentials(all rows, all sigmas) + exchange V + GGD(succ, centers, labels) "
+                               "+ labels of every sigma on every rank"},
             "breakdown_ms": dict(breakdown, wall_s_timed_region=wall),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,
@@ -419,31 +414,38 @@ def e2e_leg(args, N, torch, dist, off, nbr, sig, rank, world, dev, stream, begin
                 "d2h_bytes_per_step": int(ci.nbytes + k.nbytes),
                 "api": "gqc_cluster_sweep (C-ABI, pinned host buffers; cluster_index + counts per sigma)",
                 "ms_per_step": t * 1e3}
-    # multi-GPU: per rank, H2D of the CSR, its row shard, all-gather, GGD, D2H of its rows' labels
+    # multi-GPU: per rank, H2D of the CSR, its rows' potentials, all-to-all V
+    # by sigma chunk, GGD of its sigma chunk, D2H of that chunk's labels
     from paper_2305_14641_b200 import sharded
-    rows = end - begin
     d_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
     d_nbr = torch.empty(len(nbr), dtype=torch.int32, device=dev)
     dg = N.DeviceCsr.__new__(N.DeviceCsr)
     dg.n, dg.nnz, dg.W, dg.offsets, dg.nbr, dg.w = n, len(nbr), W_DEFAULT, d_off, d_nbr, None
-    shard = torch.zeros((block, S), dtype=torch.float64, device=dev)
-    full = torch.empty((world * block, S), dtype=torch.float64, device=dev)
-    center = torch.empty((S, n), dtype=torch.int32, device=dev)
-    ci = torch.empty_like(center)
-    nc = torch.empty(S, dtype=torch.int32, device=dev)
-    ws = torch.empty(N.dev_ggd_workspace(n, S), dtype=torch.uint8, device=dev)
-    out_ci = torch.empty((S, max(rows, 1)), dtype=torch.int32).pin_memory()
+    chunk = sharded.sigma_chunk(S, world)
+    center = torch.empty((chunk, n), dtype=torch.int32, device=dev)
+    ws = torch.empty(N.dev_ggd_workspace(n, chunk), dtype=torch.uint8, device=dev)
+
+    def pot_packed(b, e, send, ch, stride):
+        N.dev_potentials_packed(dg, sig, b, e, send, ch, stride, stream)
+
+    def ggd(v_chunk, ci_out, nc_out):
+        N.dev_ggd(dg, v_chunk, chunk, None, center, ci_out, nc_out, ws, stream)
+
+    with torch.cuda.stream(stream):
+        sweep = sharded.SigmaShardedSweep(n, S, rank, world, dev, pot_packed, ggd)
+    s0, s1 = sweep.s_begin, sweep.s_end
+    out_ci = torch.empty((max(s1 - s0, 1), n), dtype=torch.int32).pin_memory()
+    out_nc = torch.empty(max(s1 - s0, 1), dtype=torch.int32).pin_memory()
 
     def one():
         with torch.cuda.stream(stream):
             d_off.copy_(pin_off, non_blocking=True)
             d_nbr.copy_(pin_nbr, non_blocking=True)
-            if rows > 0:
-                N.dev_potentials(dg, sig, begin, end, shard[:rows], stream)
-            V = sharded.gather_rows(shard, n, None, full)
-            N.dev_ggd(dg, V, S, None, center, ci, nc, ws, stream)
-            if rows > 0:
-                out_ci[:, :rows].copy_(ci[:, begin:end], non_blocking=True)
+            sweep.potentials()
+            sweep.ggd(sweep.exchange())
+            if s1 > s0:
+                out_ci[: s1 - s0].copy_(sweep.ci[: s1 - s0], non_blocking=True)
+                out_nc[: s1 - s0].copy_(sweep.nc[: s1 - s0], non_blocking=True)
         stream.synchronize()
 
     one()
@@ -458,7 +460,9 @@ def e2e_leg(args, N, torch, dist, off, nbr, sig, rank, world, dev, stream, begin
     t = float(t.item())
     return {"value": float(n) * n * S / t / 1e9, "unit": UNIT,
             "h2d_bytes_per_step": int(world * (off.nbytes + nbr.nbytes)),
-            "d2h_bytes_per_step": int(4 * S * n), "api": "gqc_dev_* per rank + NCCL all-gather", "ms_per_step": t * 1e3}
+            "d2h_bytes_per_step": int(4 * S * n + 4 * S),
+            "api": "gqc_dev_* per rank + NCCL all-to-all(V); each rank downloads its sigma chunk's labels",
+            "ms_per_step": t * 1e3}
 
 
 def main():

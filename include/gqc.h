@@ -119,6 +119,17 @@ gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_s
 gqc_status gqc_dev_potentials(const gqc_csr* g, const double* sigmas, int32_t n_sigma, int32_t row_begin,
                               int32_t row_end, double* v_rows, void* stream);
 
+/* gqc_dev_potentials with the output packed in sigma chunks for a sigma-
+ * sharded exchange: sigma k of row i goes to
+ *     v_out[(k / chunk) * chunk_stride + (i - row_begin) * chunk + k % chunk],
+ * so chunk q is a node-major [rows][chunk] block at q * chunk_stride (one
+ * all-to-all then hands every rank the full rows of its own sigmas). Slots of
+ * a last, partial chunk beyond n_sigma are not written. Same potentials as
+ * gqc_dev_potentials (potential.cpp:18-37). */
+gqc_status gqc_dev_potentials_packed(const gqc_csr* g, const double* sigmas, int32_t n_sigma, int32_t row_begin,
+                                     int32_t row_end, double* v_out, int32_t chunk, int64_t chunk_stride,
+                                     void* stream);
+
 /* Scratch bytes gqc_dev_ggd needs for n nodes and n_sigma sigmas. */
 size_t gqc_dev_ggd_workspace(int32_t n, int32_t n_sigma);
 

@@ -195,7 +195,8 @@ void host_exp_table(const double* d2, long long count, const std::vector<double>
 // (device), for a device-resident CSR. host_w: the same weights on the host
 // (only consulted for weighted graphs), or nullptr to fetch what is needed.
 void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S, int row_begin, int row_end,
-                    double* v_nm, const double* host_w, cudaStream_t st, const std::int64_t* host_off = nullptr) {
+                    double* v_nm, const double* host_w, cudaStream_t st, const std::int64_t* host_off = nullptr,
+                    int out_chunk = 0, long long out_chunk_stride = 0) {
     const int n = g.n;
     const int mode = g_opt.exp_mode;
     const bool weighted = g.w != nullptr;
@@ -254,8 +255,10 @@ void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S,
         P.w = g.w;
         P.tail = tail ? 1 : 0;
         P.out = v_nm;
-        P.out_ld = S;
         P.out_col0 = s0;
+        P.out_chunk = out_chunk > 0 ? out_chunk : S;  // packed sigma chunks, or plain rows of S
+        P.out_ld = P.out_chunk;
+        P.out_chunk_stride = out_chunk > 0 ? out_chunk_stride : 0;
         std::vector<double> neg_inv(Sc);
         for (int s = 0; s < Sc; ++s) {
             P.c[s] = make_sigma_consts(sigmas[s0 + s], g.W, mode);
@@ -567,6 +570,24 @@ gqc_status gqc_dev_potentials(const gqc_csr* g, const double* sigmas, int32_t n_
         if (!v_rows && row_end > row_begin) fail(GQC_EINVAL, "null output");
         DeviceCtx& C = ctx();
         run_potentials(C, *g, sigmas, n_sigma, row_begin, row_end, v_rows, nullptr, static_cast<cudaStream_t>(stream));
+    });
+}
+
+gqc_status gqc_dev_potentials_packed(const gqc_csr* g, const double* sigmas, int32_t n_sigma, int32_t row_begin,
+                                     int32_t row_end, double* v_out, int32_t chunk, int64_t chunk_stride,
+                                     void* stream) {
+    return guarded([&] {
+        check_sigmas(sigmas, n_sigma);
+        check_csr_shape(g);
+        if (row_begin < 0 || row_end > g->n || row_begin > row_end) fail(GQC_ERANGE, "row range out of range");
+        if (!v_out && row_end > row_begin) fail(GQC_EINVAL, "null output");
+        if (chunk < 1) fail(GQC_EINVAL, "sigma chunk must be positive");
+        const int chunks = (n_sigma + chunk - 1) / chunk;
+        if (chunks > 1 && chunk_stride < static_cast<int64_t>(row_end - row_begin) * chunk)
+            fail(GQC_EINVAL, "chunk stride smaller than one chunk");
+        DeviceCtx& C = ctx();
+        run_potentials(C, *g, sigmas, n_sigma, row_begin, row_end, v_out, nullptr, static_cast<cudaStream_t>(stream),
+                       nullptr, chunk, chunk_stride);
     });
 }
 

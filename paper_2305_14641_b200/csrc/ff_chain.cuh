@@ -228,6 +228,92 @@ GQC_HD inline void ff_run2(Chain& a, const double ca, Chain& b, const double cb,
 }
 
 // ---------------------------------------------------------------------------
+// Batched walk over neighbour events (unit weights). Event q of a chunk is the
+// run of W terms over columns [pos, col(q)) followed by one neighbour term c1
+// at column col(q) (columns strictly ascending, pos <= col(first)). Inside a
+// binade [base, top) of s in which both c and c1 are jumpable (< base/2) and
+// neither is a half-ulp tie, every add is an exact u-grid increment, so the
+// sum after event q is exactly
+//     s + A(q) * inc + B(q) * inc1,   A = W columns up to col(q), B = events,
+// as long as that value stays below top (two exact fmas; the "< top" test is
+// exact even when it fails because rounding is monotone). The value is
+// monotone in q, so a binary search finds the last event that stays in the
+// binade; everything before it is applied at once and the next event crosses
+// (with max_steps inside its W run, or at its neighbour add). Binades where
+// the batch rule does not hold are walked one event at a time with ff_run.
+// The work per chunk is O((crossings + 1) * log(events)) instead of one
+// fast-forward per event.
+// ---------------------------------------------------------------------------
+#ifndef GQC_WALK_COUNT
+#define GQC_WALK_COUNT()
+#endif
+template <class Cols>
+GQC_HD inline double walk_events(double s, const double c, const double c1, const int tie_c, const int tie_c1,
+                                 const Cols& col, int e, const int end, int pos) {
+    while (e < end) {
+        GQC_WALK_COUNT();
+        const int f = gqc_max(exp_field(s), 1);
+        const double base = pow2_field(f);
+        const double top = gqc_add(base, base);
+        const double half = gqc_mul(base, 0.5);
+        if (c < half && c1 < half && f != tie_c && f != tie_c1) {
+            const double inc = gqc_sub(gqc_add(base, c), base);
+            const double inc1 = gqc_sub(gqc_add(base, c1), base);
+            int lo = e - 1, hi = end - 1;  // last event whose sum stays below top (e - 1: none)
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                const double t = gqc_fma(static_cast<double>(mid - e + 1), inc1,
+                                         gqc_fma(static_cast<double>(col(mid) - pos - (mid - e)), inc, s));
+                if (t < top) lo = mid;
+                else hi = mid - 1;
+            }
+            if (lo >= e) {
+                const int cl = col(lo);
+                s = gqc_fma(static_cast<double>(lo - e + 1), inc1,
+                            gqc_fma(static_cast<double>(cl - pos - (lo - e)), inc, s));
+                pos = cl + 1;
+                e = lo + 1;
+                if (e == end) break;
+            }
+            // event e leaves the binade: inside its W run or at its neighbour add
+            const int ce = col(e);
+            const int L = ce - pos;
+            const double t = gqc_fma(static_cast<double>(L), inc, s);
+            if (t < top) {
+                s = t;
+            } else {
+                Chain ch;
+                ch.s = s;
+                ch.top = top;
+                ch.inc = inc;
+                ch.f_tie = tie_c;
+                ch.flags = kJump;
+                const double m = max_steps(ch, room_of(ch));
+                ch.s = gqc_add(gqc_fma(m, inc, s), c);
+                ch.top = 0.0;
+                ff_run(ch, c, L - static_cast<int>(m) - 1);
+                s = ch.s;
+            }
+            s = gqc_add(s, c1);
+            pos = ce + 1;
+            ++e;
+        } else {  // one event at a time (tiny sums, tie binades)
+            const int ce = col(e);
+            if (ce > pos) {
+                Chain ch = make_chain(s, c);
+                ch.f_tie = tie_c;
+                ff_run(ch, c, ce - pos);
+                s = ch.s;
+            }
+            s = gqc_add(s, c1);
+            pos = ce + 1;
+            ++e;
+        }
+    }
+    return s;
+}
+
+// ---------------------------------------------------------------------------
 // Prefix segments of the pure trajectory P(t) = t sequential adds of c from
 // s = 0 (every row's first run, before its first neighbour or itself, is such
 // a run). Segment k covers [t[k], t[k+1]) with P(t) = s0[k] + (t - t[k])*inc[k]

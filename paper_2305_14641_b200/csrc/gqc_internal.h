@@ -44,8 +44,13 @@ struct PotentialLaunch {
     const double* entry_exp;   // kEntryTable: [nnz][entry_ld] at column entry_col0 + s
     std::int32_t entry_ld, entry_col0;
     const double* tail_exp;    // kDevicePexp && tail: [deg(n-1)][n_sigma] glibc exp of row n-1's entries
-    double* out;               // out[(i - row_begin) * out_ld + out_col0 + s]
+    // out[(k / out_chunk) * out_chunk_stride + (i - row_begin) * out_ld + k % out_chunk],
+    // k = out_col0 + s the sigma's index in the caller's grid (out_chunk >= that
+    // grid's size: plain node-major rows)
+    double* out;
     std::int32_t out_ld, out_col0;
+    std::int32_t out_chunk;
+    long long out_chunk_stride;
     SigmaConsts c[kMaxSigmaPerLaunch];
 };
 

@@ -24,6 +24,13 @@
 
 #include "gqc_internal.h"
 
+#ifndef GQC_CONST_SMEM
+#define GQC_CONST_SMEM 1
+#endif
+#ifndef GQC_LANE_OUT_SMEM
+#define GQC_LANE_OUT_SMEM 1
+#endif
+
 namespace gqc {
 namespace {
 
@@ -176,6 +183,13 @@ __device__ __forceinline__ void first_run(Chain& ch, const double c, const Prefi
 // (neighbours and the row itself); K2 takes the first run from the prefix
 // table and every later run through the two-chain fast-forward.
 // ---------------------------------------------------------------------------
+// Output slot of row i, launch sigma s (see PotentialLaunch::out).
+__device__ __forceinline__ long long out_index(const PotentialLaunch& P, const int i, const int s) {
+    const int k = P.out_col0 + s;
+    const int q = k / P.out_chunk;
+    return q * P.out_chunk_stride + static_cast<long long>(i - P.row_begin) * P.out_ld + (k - q * P.out_chunk);
+}
+
 template <bool kFF, int kW>
 __global__ void __launch_bounds__(kBlock) potential_kernel(const __grid_constant__ PotentialLaunch P,
                                                            const PrefixTable T) {
@@ -297,8 +311,7 @@ __global__ void __launch_bounds__(kBlock) potential_kernel(const __grid_constant
         k = kk;
         pos = end;
     }
-    P.out[static_cast<long long>(i - P.row_begin) * P.out_ld + P.out_col0 + s] =
-        __dmul_rn(sc[0][s], __ddiv_rn(num.s, den.s));
+    P.out[out_index(P, i, s)] = __dmul_rn(sc[0][s], __ddiv_rn(num.s, den.s));
 }
 
 // ---------------------------------------------------------------------------
@@ -337,7 +350,17 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
     constexpr unsigned kFull = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int s = min(lane, S - 1);  // lanes >= S shadow the last sigma (uniform walk)
+#if GQC_CONST_SMEM
+    // per-sigma constants re-read from shared memory at each use (volatile:
+    // not hoisted into registers; the unit kernel is register-bound)
+    const volatile double* vsc = &sc[0][0];
+#define pW (vsc[3 * kMaxSigmaPerLaunch + s])
+#define eW (vsc[2 * kMaxSigmaPerLaunch + s])
+#define e1 (vsc[4 * kMaxSigmaPerLaunch + s])
+#define p1 (vsc[5 * kMaxSigmaPerLaunch + s])
+#else
     const double pW = sc[3][s], eW = sc[2][s], e1 = sc[4][s], p1 = sc[5][s];
+#endif
     const int tie_num = tie_binade(pW), tie_den = tie_binade(eW);
     const int n = P.n;
     const bool tail = P.tail != 0;
@@ -375,6 +398,14 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
         }
     };
 
+#if GQC_LANE_OUT_SMEM
+    __shared__ long long lane_out_s[32];
+    if (threadIdx.x < 32) lane_out_s[threadIdx.x] = out_index(P, P.row_begin, threadIdx.x);
+    __syncthreads();
+#define lane_out (lane_out_s[lane])
+#else
+    const long long lane_out = out_index(P, P.row_begin, lane);  // this lane's sigma slot of row_begin
+#endif
     const int nrows = R.limit ? *R.limit : P.row_end - P.row_begin;
     int grab = 0, left = 0;
     for (;;) {
@@ -458,10 +489,15 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
             }
         }
         if (lane < S)
-            P.out[static_cast<long long>(i - P.row_begin) * P.out_ld + P.out_col0 + lane] =
+            P.out[lane_out + static_cast<long long>(i - P.row_begin) * P.out_ld] =
                 __dmul_rn(sc[0][s], __ddiv_rn(num.s, den.s));
     }
 }
+#undef pW
+#undef eW
+#undef e1
+#undef p1
+#undef lane_out
 
 // ---------------------------------------------------------------------------
 // K3: successor = lexicographic (v, id) argmin over the closed neighbourhood

@@ -77,6 +77,7 @@ def _load():
         "gqc_resolve_centers": [i32, P, P, P, P],
         "gqc_cluster_sweep": [P, P, i32, P, P, P, P, P],
         "gqc_dev_potentials": [P, P, i32, i32, i32, P, P],
+        "gqc_dev_potentials_packed": [P, P, i32, i32, i32, P, i32, i64, P],
         "gqc_dev_ggd": [P, P, i32, P, P, P, P, P, C.c_size_t, P],
         "gqc_dev_transpose": [P, i32, i32, P, P],
         "gqc_dev_successors": [P, P, i32, i32, i32, P, P],
@@ -295,6 +296,18 @@ def dev_potentials(dg: DeviceCsr, sigmas, row_begin: int, row_end: int, out, str
     sp = None if stream is None else C.c_void_p(stream.cuda_stream)
     _check(_lib.gqc_dev_potentials(C.byref(cs), _ptr(s), len(s), int(row_begin), int(row_end),
                                    C.c_void_p(out.data_ptr()), sp))
+
+
+def dev_potentials_packed(dg: DeviceCsr, sigmas, row_begin: int, row_end: int, out, chunk: int, chunk_stride: int,
+                          stream=None):
+    """V rows [row_begin, row_end) packed in sigma chunks: sigma k of row i at
+    out.flat[(k // chunk) * chunk_stride + (i - row_begin) * chunk + k % chunk]
+    (float64 device tensor), the send layout of the sigma-sharded exchange."""
+    s = np.ascontiguousarray(np.atleast_1d(np.asarray(sigmas, dtype=np.float64)))
+    cs = dg.c_struct()
+    sp = None if stream is None else C.c_void_p(stream.cuda_stream)
+    _check(_lib.gqc_dev_potentials_packed(C.byref(cs), _ptr(s), len(s), int(row_begin), int(row_end),
+                                          C.c_void_p(out.data_ptr()), int(chunk), int(chunk_stride), sp))
 
 
 def dev_ggd_workspace(n: int, n_sigma: int) -> int:

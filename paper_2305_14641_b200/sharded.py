@@ -1,4 +1,4 @@
-"""Row-sharded sweep over several GPUs (one process per GPU, torch.distributed).
+"""Sharded sweep over several GPUs (one process per GPU, torch.distributed).
 
 The potential of row i depends only on row i of the CSR (potential.cpp:18-37),
 so the sweep shards by rows with the full CSR replicated on every rank and no
@@ -7,6 +7,13 @@ communication while it runs. GGD needs every neighbour's potential
 (fp64, node-major [rows][n_sigma]) over NVLink, after which every rank runs
 GGD on the full field, so labels are identical on all ranks without a second
 collective.
+
+SigmaShardedSweep is the production schedule: potentials stay row-sharded,
+but the exchange hands every rank the full rows of its own sigma chunk (one
+all-to-all of V, 1/world of the all-gather's bytes), GGD then runs on that
+chunk only (every sigma's GGD is independent, ggd.cpp:7-57), and one
+all-gather assembles the labels. ShardedSweep (all-gather V, row-sharded
+successors, replicated resolve) is kept as the simpler schedule.
 
 The host logic here is device-agnostic (it takes the compute step as a
 callable) so the partition/gather/assembly path is tested on CPU with gloo.
@@ -100,3 +107,76 @@ class ShardedSweep:
         V = self.potentials()
         succ = self.successors(V)
         return V, succ, self.resolve(succ)
+
+
+def sigma_chunk(n_sigma: int, world: int) -> int:
+    """Sigmas per rank in the sigma-sharded GGD (the last chunks are padded)."""
+    return (n_sigma + world - 1) // world
+
+
+def sigma_shard(n_sigma: int, world: int, rank: int) -> Tuple[int, int]:
+    """Rank `rank` labels sigmas [begin, end) of the grid."""
+    c = sigma_chunk(n_sigma, world)
+    begin = min(n_sigma, rank * c)
+    return begin, min(n_sigma, begin + c)
+
+
+class SigmaShardedSweep:
+    """One multi-GPU step with the GGD sharded by sigma:
+
+        potentials of own rows, all sigmas (written packed by sigma chunk) ->
+        all-to-all: rank q receives every rank's rows of sigma chunk q ->
+        GGD (successors, centers, labels) of sigma chunk q over all rows ->
+        all-gather of the labels [S][n] and counts [S]
+
+    Bytes on the wire per rank: (world-1)/world * n*S*8/world for V plus the
+    labels gather, against (world-1)/world * n*S*(8+4) for all-gather(V) +
+    all-gather(succ); and no rank repeats another's GGD work.
+
+      potentials_packed(begin, end, send, chunk, chunk_stride): V rows
+          [begin, end) into the flat send buffer, sigma k of row i at
+          (k // chunk) * chunk_stride + (i - begin) * chunk + k % chunk
+      ggd(V_chunk [n, chunk] node-major, ci [chunk, n] int32, nc [chunk] int32)
+    Padding (rows past n, sigmas past S) stays zero and is dropped.
+    """
+
+    def __init__(self, n, n_sigma, rank, world, device, potentials_packed, ggd, group=None):
+        self.n, self.S, self.rank, self.world, self.group = n, n_sigma, rank, world, group
+        self.block = row_block(n, world)
+        self.begin, self.end = row_shard(n, world, rank)
+        self.chunk = sigma_chunk(n_sigma, world)
+        self.s_begin, self.s_end = sigma_shard(n_sigma, world, rank)
+        self.potentials_packed, self.ggd_op = potentials_packed, ggd
+        cells = world * self.block * self.chunk
+        self.send = torch.zeros(cells, dtype=torch.float64, device=device)
+        self.recv = torch.zeros(cells, dtype=torch.float64, device=device) if world > 1 else self.send
+        self.ci = torch.zeros((self.chunk, n), dtype=torch.int32, device=device)
+        self.nc = torch.zeros(self.chunk, dtype=torch.int32, device=device)
+        self.ci_full = torch.empty((world * self.chunk, n), dtype=torch.int32, device=device) if world > 1 else self.ci
+        self.nc_full = torch.empty(world * self.chunk, dtype=torch.int32, device=device) if world > 1 else self.nc
+
+    def potentials(self):
+        if self.end > self.begin:
+            self.potentials_packed(self.begin, self.end, self.send, self.chunk, self.block * self.chunk)
+
+    def exchange(self):
+        """V of this rank's sigma chunk for all rows, node-major [n, chunk]."""
+        if self.world > 1:
+            dist.all_to_all_single(self.recv, self.send, group=self.group)
+        return self.recv.view(self.world * self.block, self.chunk)[: self.n]
+
+    def ggd(self, v_chunk):
+        self.ggd_op(v_chunk, self.ci, self.nc)
+
+    def gather(self):
+        """Labels [S, n] and counts [S] of the whole grid on every rank."""
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.ci_full, self.ci, group=self.group)
+            dist.all_gather_into_tensor(self.nc_full, self.nc, group=self.group)
+        return self.ci_full[: self.S], self.nc_full[: self.S]
+
+    def step(self):
+        self.potentials()
+        v = self.exchange()
+        self.ggd(v)
+        return self.gather()

@@ -5,7 +5,12 @@
 // Built by tests/test_ff_cpu.py with g++ -O2 -ffp-contract=off (no -march).
 #include <cstdint>
 #include <cstring>
+#include <algorithm>
+#include <cmath>
+#include <vector>
 
+static thread_local long long g_walk_iters = 0;
+#define GQC_WALK_COUNT() (++g_walk_iters)
 #include "ff_chain.cuh"
 
 using namespace gqc::ffc;
@@ -244,4 +249,93 @@ double fft_run(double s, double c, int L) {
 
 double fft_naive(double s, double c, long long L) { return naive(s, c, L); }
 
+
+// One accumulator of a unit-weight row through walk_events (neighbours before
+// the row's own column, the self term, neighbours after it, the final run),
+// as the batched kernel walks it.
+static double walk_row(double c, double c1, double cself, const int* nb, int deg, int self, int ncols) {
+    struct Cols {
+        const int* p;
+        int operator()(int q) const { return p[q]; }
+    } col{nb};
+    const int tc = tie_binade(c), tc1 = tie_binade(c1);
+    int k1 = 0;
+    while (k1 < deg && nb[k1] < self) ++k1;
+    double s = walk_events(0.0, c, c1, tc, tc1, col, 0, k1, 0);
+    int pos = k1 ? nb[k1 - 1] + 1 : 0;
+    Chain ch = make_chain(s, c);
+    ff_run(ch, c, self - pos);
+    s = ch.s + cself;
+    s = walk_events(s, c, c1, tc, tc1, col, k1, deg, self + 1);
+    pos = deg > k1 ? nb[deg - 1] + 1 : self + 1;
+    ch = make_chain(s, c);
+    ff_run(ch, c, ncols - pos);
+    return ch.s;
+}
+
+static double naive_row(double c, double c1, double cself, const int* nb, int deg, int self, int ncols) {
+    double s = 0.0;
+    int k = 0;
+    for (int j = 0; j < ncols; ++j) {
+        if (j == self) s = s + cself;
+        else if (k < deg && nb[k] == j) s = s + c1, ++k;
+        else s = s + c;
+    }
+    return s;
+}
+
+// Random rows (degree, neighbour columns, self), random constants with tie-prone
+// mantissas plus the QC constants of random sigmas; both accumulators. Returns
+// mismatches; bad = (c, c1, row). iters_out (optional) = walk iterations.
+long long fft_walk(std::uint64_t seed, int nrows, int ncols, double* bad, long long* iters_out) {
+    Rng r{seed};
+    long long mism = 0;
+    std::vector<int> nb;
+    g_walk_iters = 0;
+    for (int row = 0; row < nrows; ++row) {
+        const int deg = r.below(4) == 0 ? r.below(400) : r.below(40);
+        const int self = r.below(ncols);
+        nb.clear();
+        for (int q = 0; q < deg; ++q) {
+            const int j = r.below(ncols);
+            if (j != self) nb.push_back(j);
+        }
+        std::sort(nb.begin(), nb.end());
+        nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
+        double c, c1;
+        if (r.below(2)) {
+            const double sigma = 0.05 + 40.0 * r.uni();
+            const double inv = 1.0 / (2.0 * sigma * sigma);
+            c = std::exp(-inv * 100.0);
+            c1 = std::exp(-inv);
+            if (r.below(2)) c = 100.0 * c, c1 = 1.0 * c1;  // numerator constants
+        } else {
+            const int ec = 1 + r.below(1060);
+            c = rand_double(r, ec, ec);
+            c1 = rand_double(r, ec + r.below(45), ec + 45);
+            if (r.below(8) == 0) c1 = c;
+        }
+        const double cself = r.below(2) ? 1.0 : 0.0;
+        const double got = walk_row(c, c1, cself, nb.data(), static_cast<int>(nb.size()), self, ncols);
+        const double ref = naive_row(c, c1, cself, nb.data(), static_cast<int>(nb.size()), self, ncols);
+        if (std::memcmp(&got, &ref, sizeof ref) != 0) {
+            if (mism == 0 && bad) {
+                bad[0] = c;
+                bad[1] = c1;
+                bad[2] = row;
+            }
+            ++mism;
+        }
+    }
+    if (iters_out) *iters_out = g_walk_iters;
+    return mism;
+}
+
 }  // extern "C"
+
+extern "C" long long fft_walk_row_iters(double c, double c1, double cself, const int* nb, int deg, int self,
+                                        int ncols, double* out) {
+    g_walk_iters = 0;
+    *out = walk_row(c, c1, cself, nb, deg, self, ncols);
+    return g_walk_iters;
+}

@@ -74,3 +74,13 @@ def test_two_chain_rows_with_prefix_bitwise(ff, seed):
     bad = np.zeros(3)
     m = ff.fft_rows2(seed, 3000, 20000, bad.ctypes.data_as(C.c_void_p))
     assert m == 0, f"{m} mismatches, first (e, term, row) = {bad.tolist()}"
+
+
+@pytest.mark.parametrize("seed,ncols", [(21, 200000), (22, 200000), (23, 60), (24, 7), (25, 5000)])
+def test_batched_row_walk_bitwise(ff, seed, ncols):
+    # walk_events (batched in-binade jumps over neighbour events) vs naive adds
+    ff.fft_walk.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+    ff.fft_walk.restype = C.c_longlong
+    bad = np.zeros(3)
+    m = ff.fft_walk(seed, 2000, ncols, bad.ctypes.data_as(C.c_void_p), None)
+    assert m == 0, f"{m} mismatches, first (c, c1, row) = {bad.tolist()}"

@@ -272,6 +272,57 @@ def test_device_api_row_shards_assemble_to_full_field():
     assert nc.cpu().tolist() == [r.num_clusters for r in res]
 
 
+@pytest.mark.parametrize("S,chunk", [(32, 32), (32, 8), (32, 4), (13, 5), (9, 1), (40, 7)])
+@pytest.mark.parametrize("unit", [True, False])
+def test_packed_potentials_are_a_rearrangement(S, chunk, unit):
+    # gqc_dev_potentials_packed: sigma k of row i at (k // chunk) * stride +
+    # (i - begin) * chunk + k % chunk, bit-identical to the node-major field;
+    # padding slots of the last chunk are untouched
+    import torch
+    g = H.random_graph(3001, 6.0, seed=5, unit=unit)
+    dg = N.DeviceCsr(g.csr(N))
+    sig = O.log_sigma_grid(10.0, S)
+    b, e = 1000, 2500
+    full = torch.empty((e - b, S), dtype=torch.float64, device="cuda")
+    N.dev_potentials(dg, sig, b, e, full)
+    q = (S + chunk - 1) // chunk
+    stride = (e - b) * chunk + 3
+    packed = torch.full((q * stride,), -7.0, dtype=torch.float64, device="cuda")
+    N.dev_potentials_packed(dg, sig, b, e, packed, chunk, stride)
+    torch.cuda.synchronize()
+    f, p = full.cpu().numpy(), packed.cpu().numpy()
+    for k in range(q):
+        blk = p[k * stride: k * stride + (e - b) * chunk].reshape(e - b, chunk)
+        real = min(chunk, S - k * chunk)
+        assert np.array_equal(blk[:, :real].view(np.int64), f[:, k * chunk: k * chunk + real].view(np.int64))
+        assert np.all(blk[:, real:] == -7.0)
+        assert np.all(p[k * stride + (e - b) * chunk: (k + 1) * stride] == -7.0)
+    with pytest.raises(ValueError):
+        N.dev_potentials_packed(dg, sig, b, e, packed, 0, stride)
+
+
+def test_sigma_sharded_schedule_single_gpu_matches_cluster_sweep():
+    # SigmaShardedSweep at world 1 (the bench schedule) through the device API
+    import torch
+    from paper_2305_14641_b200 import sharded
+    g = H.random_graph(4000, 7.0, seed=8, unit=True)
+    csr = g.csr(N)
+    dg = N.DeviceCsr(csr)
+    sig = O.log_sigma_grid(10.0, 32)
+    S = len(sig)
+    center = torch.empty((S, g.n), dtype=torch.int32, device="cuda")
+    ws = torch.empty(N.dev_ggd_workspace(g.n, S), dtype=torch.uint8, device="cuda")
+    sweep = sharded.SigmaShardedSweep(
+        g.n, S, 0, 1, "cuda",
+        lambda b, e, send, ch, st: N.dev_potentials_packed(dg, sig, b, e, send, ch, st),
+        lambda v, ci, nc: N.dev_ggd(dg, v, S, None, center, ci, nc, ws))
+    ci, nc = sweep.step()
+    torch.cuda.synchronize()
+    res, _, _ = N.cluster_sweep(csr, sig)
+    assert np.array_equal(ci.cpu().numpy(), np.stack([r.cluster_index for r in res]))
+    assert nc.cpu().tolist() == [r.num_clusters for r in res]
+
+
 def _dev_labels(g_csr, sig):
     import torch
     dg = N.DeviceCsr(g_csr)

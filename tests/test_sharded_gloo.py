@@ -112,3 +112,64 @@ def test_gloo_sharded_ggd_matches_single_process(world, tmp_path):
                        start_method="spawn")
     for r in range(world):
         assert (tmp_path / f"r.{r}").read_text() == "ok"
+
+
+def test_sigma_shards_partition_the_grid():
+    for S in (1, 3, 7, 32, 33):
+        for world in (1, 2, 3, 4, 8):
+            got = [sharded.sigma_shard(S, world, r) for r in range(world)]
+            assert got[0][0] == 0 and got[-1][1] == S
+            for (a, b), (c, d) in zip(got[:-1], got[1:]):
+                assert b == c and a <= b
+            assert all(b - a <= sharded.sigma_chunk(S, world) for a, b in got)
+
+
+def _worker_sigma(rank, world, port, result_path, n_nodes, sig):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import pyoracle as O
+        from tests import helpers as H
+        g = H.random_graph(n_nodes, 3.0, seed=13, unit=True)
+        S = len(sig)
+
+        def potentials_packed(begin, end, send, chunk, stride):
+            rows = np.arange(begin, end, dtype=np.int32)
+            for k, s in enumerate(sig):
+                q, r = divmod(k, chunk)
+                v = torch.from_numpy(O.potentials_rows(g.offsets, g.nbr, g.wt, 10.0, s, rows))
+                send[q * stride + r: q * stride + r + (end - begin) * chunk: chunk] = v
+
+        def ggd(V, ci, nc):
+            for k in range(V.shape[1]):
+                succ = O.build_successors(g.offsets, g.nbr, V[:, k].numpy().copy())
+                _, cik, kk = O.resolve_centers(succ)
+                ci[k] = torch.from_numpy(cik)
+                nc[k] = kk
+
+        sweep = sharded.SigmaShardedSweep(g.n, S, rank, world, "cpu", potentials_packed, ggd)
+        ci, nc = sweep.step()
+        ok = tuple(ci.shape) == (S, g.n) and tuple(nc.shape) == (S,)
+        for q, s in enumerate(sig):
+            _, _, _, cio, ko = O.cluster(g.offsets, g.nbr, g.wt, 10.0, s)
+            ok &= np.array_equal(ci[q].numpy(), cio) and int(nc[q]) == ko
+        with open(f"{result_path}.{rank}", "w") as f:
+            f.write("ok" if ok else "mismatch")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_nodes,sig", [(2, 97, [0.7, 2.3, 5.0, 30.0]),
+                                               (3, 101, [0.7, 2.3, 5.0, 9.0, 30.0]),  # padded sigma chunk
+                                               (3, 2, [1.0, 4.0]),                     # fewer rows / sigmas than ranks
+                                               (2, 64, [3.0])])                        # one rank with no sigma
+def test_gloo_sigma_sharded_ggd_matches_single_process(world, n_nodes, sig, tmp_path):
+    # the production multi-GPU schedule: row-sharded potentials -> all-to-all of
+    # V by sigma chunk -> per-chunk GGD -> all-gather labels; every rank ends
+    # with the single-process labels of every sigma
+    result = tmp_path / "r"
+    mp.start_processes(_worker_sigma, args=(world, _free_port(), str(result), n_nodes, sig), nprocs=world,
+                       join=True, start_method="spawn")
+    for r in range(world):
+        assert (tmp_path / f"r.{r}").read_text() == "ok"
