@@ -260,6 +260,11 @@ GQC_HD inline double walk_events(double s, const double c, const double c1, cons
             const double inc = gqc_sub(gqc_add(base, c), base);
             const double inc1 = gqc_sub(gqc_add(base, c1), base);
             int lo = e - 1, hi = end - 1;  // last event whose sum stays below top (e - 1: none)
+            {  // common case: the rest of the range stays in the binade
+                const double t = gqc_fma(static_cast<double>(end - e), inc1,
+                                         gqc_fma(static_cast<double>(col(end - 1) - pos - (end - 1 - e)), inc, s));
+                if (t < top) lo = hi;
+            }
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
                 const double t = gqc_fma(static_cast<double>(mid - e + 1), inc1,

@@ -322,7 +322,12 @@ __global__ void __launch_bounds__(kBlock) potential_kernel(const __grid_constant
 // read back with shuffles; the prefix search keys live in shared memory.
 // Persistent: each warp strides over rows.
 // ---------------------------------------------------------------------------
-constexpr int kPrefixStride = kPrefixCap + 1;  // padded: no bank conflicts across lanes
+constexpr int kPrefixStride = kPrefixCap + 1;
+// Rows with at least this many neighbours take the batched walk (unit weights).
+#ifndef GQC_BATCH_MIN_DEGREE
+#define GQC_BATCH_MIN_DEGREE 32
+#endif
+constexpr int kBatchMinDegree = GQC_BATCH_MIN_DEGREE;  // padded: no bank conflicts across lanes
 
 template <bool kFF, int kW>
 __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp_kernel(const __grid_constant__ PotentialLaunch P,
@@ -330,6 +335,7 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
     __shared__ double sc[kSigmaFields][kMaxSigmaPerLaunch];
     __shared__ int pt[kFF ? 2 * kMaxSigmaPerLaunch * kPrefixStride : 1];
     __shared__ int pcount[2 * kMaxSigmaPerLaunch], pend[2 * kMaxSigmaPerLaunch];
+    __shared__ int batch_cols[(kFF && kW == kUnit) ? kBlock : 1];  // per-warp neighbour chunk (batched rows)
     const int S = P.n_sigma;
     for (int idx = threadIdx.x; idx < kSigmaFields * kMaxSigmaPerLaunch; idx += blockDim.x) {
         const int ss = idx % kMaxSigmaPerLaunch, f = idx / kMaxSigmaPerLaunch;
@@ -426,50 +432,108 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
         den.s = 0.0; den.top = 0.0; den.inc = 0.0; den.f_tie = tie_den; den.flags = 0;
         int pos = 0;              // first column not yet added
         bool self_pending = true;
-        // neighbours in chunks of 32: one coalesced load, then shuffles
-        for (long long base = kbeg; base < kend; base += 32) {
-            const int cnt = static_cast<int>(min(32ll, kend - base));
-            const int my = lane < cnt ? __ldg(P.nbr + base + lane) : n;
-            double myw = 1.0;
-            if constexpr (kW != kUnit) myw = lane < cnt ? __ldg(P.w + base + lane) : 1.0;
-            for (int j = 0; j < cnt; ++j) {
-                const int col = __shfl_sync(kFull, my, j);
-                if (self_pending && i < col) {  // the row's own column precedes this neighbour
-                    w_run(num, den, pos, i - pos);
-                    den.s = __dadd_rn(den.s, 1.0);  // self: num += 0, den += 1
-                    pos = i + 1;
-                    self_pending = false;
-                }
-                w_run(num, den, pos, col - pos);
-                const bool at_tail = tail && col == n - 1;
-                double e, p;
-                if constexpr (kW == kUnit) {
-                    e = at_tail ? sc[8][s] : e1;
-                    p = at_tail ? sc[9][s] : p1;
+        // one neighbour event: the W run up to col (and the row's own column if
+        // it comes first), then the neighbour term of CSR entry k (weight wk)
+        auto event = [&](const int col, const long long k, const double wk) {
+            if (self_pending && i < col) {  // the row's own column precedes this neighbour
+                w_run(num, den, pos, i - pos);
+                den.s = __dadd_rn(den.s, 1.0);  // self: num += 0, den += 1
+                pos = i + 1;
+                self_pending = false;
+            }
+            w_run(num, den, pos, col - pos);
+            const bool at_tail = tail && col == n - 1;
+            double e, p;
+            if constexpr (kW == kUnit) {
+                e = at_tail ? sc[8][s] : e1;
+                p = at_tail ? sc[9][s] : p1;
+            } else {
+                const double d2 = __dmul_rn(wk, wk);
+                if constexpr (kW == kEntryTable) {
+                    e = __ldg(P.entry_exp + k * P.entry_ld + P.entry_col0 + s);
                 } else {
-                    const double wk = __shfl_sync(kFull, myw, j);
-                    const double d2 = __dmul_rn(wk, wk);
-                    if constexpr (kW == kEntryTable) {
-                        e = __ldg(P.entry_exp + (base + j) * P.entry_ld + P.entry_col0 + s);
-                    } else {
-                        if (at_tail) {  // glibc value, stored in row n-1's entry order
-                            long long lo = P.offsets[n - 1], hi = P.offsets[n];
-                            const long long b0 = lo;
-                            while (lo < hi) {
-                                const long long mid = (lo + hi) >> 1;
-                                if (__ldg(P.nbr + mid) < i) lo = mid + 1;
-                                else hi = mid;
-                            }
-                            e = __ldg(P.tail_exp + (lo - b0) * S + s);
-                        } else {
-                            e = pexp_dev(__dmul_rn(sc[1][s], d2));
+                    if (at_tail) {  // glibc value, stored in row n-1's entry order
+                        long long lo = P.offsets[n - 1], hi = P.offsets[n];
+                        const long long b0 = lo;
+                        while (lo < hi) {
+                            const long long mid = (lo + hi) >> 1;
+                            if (__ldg(P.nbr + mid) < i) lo = mid + 1;
+                            else hi = mid;
                         }
+                        e = __ldg(P.tail_exp + (lo - b0) * S + s);
+                    } else {
+                        e = pexp_dev(__dmul_rn(sc[1][s], d2));
                     }
-                    p = __dmul_rn(d2, e);
                 }
-                num.s = __dadd_rn(num.s, p);
-                den.s = __dadd_rn(den.s, e);
-                pos = col + 1;
+                p = __dmul_rn(d2, e);
+            }
+            num.s = __dadd_rn(num.s, p);
+            den.s = __dadd_rn(den.s, e);
+            pos = col + 1;
+        };
+        bool batched = false;
+        if constexpr (kFF && kW == kUnit) batched = kend - kbeg >= kBatchMinDegree;
+        if (batched) {
+            // High-degree rows: each 32-neighbour chunk is staged in shared
+            // memory and every accumulator walks it with walk_events (batched
+            // exact in-binade jumps, ff_chain.cuh). The row's first event
+            // (prefix-table run), its own column and a tail neighbour (column
+            // n-1 of an odd-N graph) keep the per-event path.
+            int* cols = batch_cols + (threadIdx.x >> 5) * 32;
+            const struct {
+                const int* c;
+                __device__ int operator()(int q) const { return c[q]; }
+            } colf{cols};
+            const int tie_p1 = tie_binade(p1), tie_e1 = tie_binade(e1);
+            auto walk = [&](const int j0, const int j1) {
+                num.s = walk_events(num.s, pW, p1, tie_num, tie_p1, colf, j0, j1, pos);
+                den.s = walk_events(den.s, eW, e1, tie_den, tie_e1, colf, j0, j1, pos);
+                num.top = 0.0;  // the chains' binade caches are stale now
+                den.top = 0.0;
+                pos = cols[j1 - 1] + 1;
+            };
+            for (long long base = kbeg; base < kend; base += 32) {
+                const int cnt = static_cast<int>(min(32ll, kend - base));
+                const int my = lane < cnt ? __ldg(P.nbr + base + lane) : n;
+                __syncwarp();
+                cols[lane] = my;
+                __syncwarp();
+                const int jend = (tail && cols[cnt - 1] == n - 1) ? cnt - 1 : cnt;
+                const int before_self = __popc(__ballot_sync(kFull, lane < cnt && my < i));
+                int j = 0;
+                while (j < cnt) {  // warp-uniform
+                    if (pos == 0 || j >= jend) {  // first event of the row, or the tail neighbour
+                        event(cols[j], base + j, 1.0);
+                        ++j;
+                        continue;
+                    }
+                    int r = jend;
+                    if (self_pending) r = min(max(before_self, j), jend);
+                    if (r > j) {
+                        walk(j, r);
+                        j = r;
+                    }
+                    if (self_pending && j < jend) {  // the row's own column comes before event j
+                        w_run(num, den, pos, i - pos);
+                        den.s = __dadd_rn(den.s, 1.0);
+                        pos = i + 1;
+                        self_pending = false;
+                    }
+                }
+            }
+        } else {
+            // neighbours in chunks of 32: one coalesced load, then shuffles
+            for (long long base = kbeg; base < kend; base += 32) {
+                const int cnt = static_cast<int>(min(32ll, kend - base));
+                const int my = lane < cnt ? __ldg(P.nbr + base + lane) : n;
+                double myw = 1.0;
+                if constexpr (kW != kUnit) myw = lane < cnt ? __ldg(P.w + base + lane) : 1.0;
+                for (int j = 0; j < cnt; ++j) {
+                    const int col = __shfl_sync(kFull, my, j);
+                    double wk = 1.0;
+                    if constexpr (kW != kUnit) wk = __shfl_sync(kFull, myw, j);
+                    event(col, base + j, wk);
+                }
             }
         }
         if (self_pending) {

@@ -422,3 +422,38 @@ def test_row_sharded_successors_and_resolve_match_full_ggd():
         assert np.array_equal(succ.cpu().numpy().T, s_ref)
         assert np.array_equal(center.cpu().numpy(), c_ref) and np.array_equal(ci.cpu().numpy(), ci_ref)
         assert nc.cpu().tolist() == nc_ref.tolist()
+
+
+def hub_graph(n, seed):
+    """Random sparse graph plus hub rows of degree 64..2000 (the batched walk):
+    hubs at columns 0 and n-1 and in the middle, hubs adjacent to n-1 (the
+    Eigen tail column when n is odd), neighbour lists spanning many 32-chunks."""
+    rng = np.random.default_rng(seed)
+    u, v, _ = H.graphgen.random_edges(n, 4.0, unit=True, seed=seed)
+    us, vs = [u], [v]
+    hubs = [0, n - 1, n // 2, n // 3 + 1, 7]
+    for h, deg in zip(hubs, [300, 2000, 64, 65, 1000]):
+        nb = rng.choice(n, size=min(deg, n - 1), replace=False)
+        nb = nb[nb != h]
+        us.append(np.full(len(nb), h, np.int32))
+        vs.append(nb.astype(np.int32))
+    # a hub whose neighbours are exactly the columns right below and above it
+    h = n // 4
+    nb = np.array([c for c in range(h - 40, h + 60) if c != h and 0 <= c < n], np.int32)
+    us.append(np.full(len(nb), h, np.int32))
+    vs.append(nb)
+    return H.G(n, np.concatenate(us), np.concatenate(vs), None, 10.0)
+
+
+@pytest.mark.parametrize("n", [4001, 4000])
+def test_batched_walk_hub_rows_bitwise(n):
+    # rows with >= 64 neighbours take the batched in-binade walk; every row of
+    # every sigma (incl. tiny and huge) must equal the oracle and the replay
+    g = hub_graph(n, seed=n)
+    assert np.diff(g.offsets).max() >= 1000
+    sig = sorted(set(list(O.log_sigma_grid(10.0, 32)) + [0.05, 0.3, 500.0]))
+    field = N.potentials(g.csr(N), sig)
+    for q, s in enumerate(sig):
+        assert_bits(field[q], oracle_field(g, s, N.EXP_EIGEN))
+    N.set_kernel(N.KERNEL_REPLAY)
+    assert_bits(N.potentials(g.csr(N), sig), field)
