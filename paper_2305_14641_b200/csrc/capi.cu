@@ -416,7 +416,7 @@ gqc_status gqc_build_successors(const gqc_csr* g, const double* v, int32_t* succ
         double* dv = C.v_nm.get<double>(g->n);
         int* ds = C.succ.get<int>(g->n);
         cuda_check(cudaMemcpyAsync(dv, v, g->n * sizeof(double), cudaMemcpyHostToDevice, st), "copy V");
-        cuda_check(launch_successors(g->n, d.offsets, d.nbr, dv, 1, 0, 1, 0, g->n, ds, 1, g->n, C.pool, st), "successor kernel");
+        cuda_check(launch_successors(g->n, d.offsets, d.nbr, dv, 1, 0, 1, 0, g->n, ds, 1, g->n, g->nnz, C.pool, st), "successor kernel");
         cuda_check(cudaMemcpyAsync(succ, ds, g->n * sizeof(int), cudaMemcpyDeviceToHost, st), "copy succ");
         cuda_check(cudaStreamSynchronize(st), "build successors");
     });
@@ -536,7 +536,7 @@ gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_s
         for (int s0 = 0; s0 < n_sigma; s0 += chunk) {
             const int Sc = std::min(chunk, n_sigma - s0);
             const std::size_t o = static_cast<std::size_t>(s0) * n, c = static_cast<std::size_t>(Sc) * n;
-            cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, s0, Sc, 0, n, ds + o, 1, n, C.pool, st), "successor kernel");
+            cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, s0, Sc, 0, n, ds + o, 1, n, nnz, C.pool, st), "successor kernel");
             cuda_check(launch_chase(n, Sc, ds + o, dc + o, st), "chase kernel");
             cuda_check(launch_labels(n, Sc, dc + o, dci + o, dnc + s0, ws, wsb, st), "label kernels");
             tr.mark("ggd_chunk");
@@ -607,7 +607,7 @@ gqc_status gqc_dev_ggd(const gqc_csr* g, const double* v, int32_t n_sigma, int32
         auto st = static_cast<cudaStream_t>(stream);
         DeviceCtx& C = ctx();
         int* s = succ ? succ : center;  // the chase runs in place on center
-        cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, 0, g->n, s, 1, g->n, C.pool, st), "successor kernel");
+        cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, 0, g->n, s, 1, g->n, g->nnz, C.pool, st), "successor kernel");
         cuda_check(launch_chase(g->n, n_sigma, s, center, st), "chase kernel");
         cuda_check(launch_labels(g->n, n_sigma, center, cluster_index, num_clusters, workspace, workspace_bytes, st),
                    "label kernels");
@@ -623,7 +623,7 @@ gqc_status gqc_dev_successors(const gqc_csr* g, const double* v, int32_t n_sigma
         if (!v || (!succ_rows && row_end > row_begin)) fail(GQC_EINVAL, "null buffer");
         DeviceCtx& C = ctx();
         cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, row_begin, row_end, succ_rows,
-                                     n_sigma, 1, C.pool, static_cast<cudaStream_t>(stream)),
+                                     n_sigma, 1, g->nnz, C.pool, static_cast<cudaStream_t>(stream)),
                    "successor kernel");
     });
 }

@@ -64,8 +64,8 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
 // (sigma-major: out_row = 1, out_col = n; node-major shard: out_row = ld, out_col = 1).
 int launch_successors(std::int32_t n, const std::int64_t* offsets, const std::int32_t* nbr, const double* v,
                       std::int32_t ld, std::int32_t s0, std::int32_t n_sigma, std::int32_t row_begin,
-                      std::int32_t row_end, std::int32_t* out, long long out_row, long long out_col, void* pool,
-                      void* stream);
+                      std::int32_t row_end, std::int32_t* out, long long out_row, long long out_col, long long nnz,
+                      void* pool, void* stream);
 int launch_transpose_i32(const std::int32_t* in, std::int32_t n, std::int32_t n_sigma, std::int32_t* out, void* stream);
 int launch_chase(std::int32_t n, std::int32_t n_sigma, const std::int32_t* succ_sm, std::int32_t* center_sm,
                  void* stream);

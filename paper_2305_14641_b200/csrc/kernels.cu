@@ -576,6 +576,15 @@ struct SuccOut {
     long long out_row, out_col;
 };
 
+#ifndef GQC_SUCC_UNROLL
+#define GQC_SUCC_UNROLL 4
+#endif
+#ifndef GQC_HEAVY_UNROLL
+#define GQC_HEAVY_UNROLL 4
+#endif
+constexpr int kSuccUnroll = GQC_SUCC_UNROLL;    // gathers in flight per thread (light rows)
+constexpr int kHeavyUnroll = GQC_HEAVY_UNROLL;  // gathers in flight per warp (heavy rows)
+
 __global__ void __launch_bounds__(kBlock) successors_kernel(const long long* __restrict__ off,
                                                             const int* __restrict__ nbr,
                                                             const double* __restrict__ v, int ld, int s0, int Sc,
@@ -590,7 +599,23 @@ __global__ void __launch_bounds__(kBlock) successors_kernel(const long long* __r
     if (kend - off[i] > kHeavyDegree) return;  // heavy rows: successors_heavy_kernel
     int best = i;
     double vb = __ldg(v + static_cast<long long>(i) * ld + s);
-    for (long long k = off[i]; k < kend; ++k) {
+    long long k = off[i];
+    // kSuccUnroll independent gathers in flight, compared in ascending k
+    for (; k + kSuccUnroll <= kend; k += kSuccUnroll) {
+        int j[kSuccUnroll];
+        double vj[kSuccUnroll];
+#pragma unroll
+        for (int u = 0; u < kSuccUnroll; ++u) j[u] = __ldg(nbr + k + u);
+#pragma unroll
+        for (int u = 0; u < kSuccUnroll; ++u) vj[u] = __ldg(v + static_cast<long long>(j[u]) * ld + s);
+#pragma unroll
+        for (int u = 0; u < kSuccUnroll; ++u)
+            if (vj[u] < vb || (vj[u] == vb && j[u] < best)) {
+                best = j[u];
+                vb = vj[u];
+            }
+    }
+    for (; k < kend; ++k) {
         const int j = __ldg(nbr + k);
         const double vj = __ldg(v + static_cast<long long>(j) * ld + s);
         if (vj < vb || (vj == vb && j < best)) {
@@ -602,13 +627,37 @@ __global__ void __launch_bounds__(kBlock) successors_kernel(const long long* __r
 }
 
 // Heavy rows (degree > kHeavyDegree, e.g. R-MAT hubs with ~10^5 neighbours)
-// are listed by a marking pass and reduced by one block each: the
-// lexicographic (v, id) minimum is associative, so a hub no longer serialises
-// on one thread.
-__global__ void mark_heavy_kernel(const long long* __restrict__ off, int row_begin, int rows, int* __restrict__ list,
-                                  int* __restrict__ count) {
+// are cut into segments of at most kHeavySegment neighbours by a marking
+// pass and every segment is reduced by one block: the lexicographic (v, id)
+// minimum is a total-order minimum (potentials are never NaN: den >= 1), so
+// partial minima combine in any order to the same successor, and a hub no
+// longer serialises on one block. Single-segment rows write their successor
+// directly; longer rows write per-segment partials that a warp per row
+// combines.
+constexpr int kHeavySegment = 2048;
+
+struct HeavyItem {
+    int row, seg, slot;  // slot: partial-minimum slot, -1 for single-segment rows
+};
+struct HeavyRow {
+    int row, slot0, nseg;
+};
+
+__global__ void mark_heavy_kernel(const long long* __restrict__ off, int row_begin, int rows,
+                                  HeavyItem* __restrict__ items, int* __restrict__ counts, HeavyRow* __restrict__ multi) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r < rows && off[row_begin + r + 1] - off[row_begin + r] > kHeavyDegree) list[atomicAdd(count, 1)] = row_begin + r;
+    if (r >= rows) return;
+    const int i = row_begin + r;
+    const long long deg = off[i + 1] - off[i];
+    if (deg <= kHeavyDegree) return;
+    const int nseg = static_cast<int>((deg + kHeavySegment - 1) / kHeavySegment);
+    const int base = atomicAdd(&counts[0], nseg);
+    int slot0 = -1;
+    if (nseg > 1) {
+        slot0 = atomicAdd(&counts[1], nseg);
+        multi[atomicAdd(&counts[2], 1)] = HeavyRow{i, slot0, nseg};
+    }
+    for (int q = 0; q < nseg; ++q) items[base + q] = HeavyItem{i, q, nseg > 1 ? slot0 + q : -1};
 }
 
 __device__ __forceinline__ bool lex_less(double va, int ia, double vb, int ib) {
@@ -618,23 +667,46 @@ __device__ __forceinline__ bool lex_less(double va, int ia, double vb, int ib) {
 __global__ void __launch_bounds__(kBlock) successors_heavy_kernel(const long long* __restrict__ off,
                                                                   const int* __restrict__ nbr,
                                                                   const double* __restrict__ v, int ld, int s0, int Sc,
-                                                                  int row_begin, const int* __restrict__ list,
-                                                                  const int* __restrict__ count, SuccOut O) {
-    // one block per heavy row: lane = sigma, the 8 warps split the neighbour
-    // list (each neighbour's potentials are one coalesced node-major line),
-    // then the per-warp minima are combined per sigma in shared memory
+                                                                  int row_begin, const HeavyItem* __restrict__ items,
+                                                                  const int* __restrict__ counts,
+                                                                  double* __restrict__ part_v, int* __restrict__ part_i,
+                                                                  SuccOut O) {
+    // one block per segment: lane = sigma, the 8 warps split the segment
+    // (each neighbour's potentials are one coalesced node-major line), then
+    // the per-warp minima are combined per sigma in shared memory
     constexpr int kWarps = kBlock / 32;
     __shared__ double sv[kWarps][32];
     __shared__ int si[kWarps][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int s = s0 + min(lane, Sc - 1);
-    const int heavy = *count;
-    for (int h = blockIdx.x; h < heavy; h += gridDim.x) {
-        const int i = list[h];
-        double vb = __ldg(v + static_cast<long long>(i) * ld + s);
-        int best = i;
-        const long long kend = off[i + 1];
-        for (long long k = off[i] + warp; k < kend; k += kWarps) {
+    const int total = counts[0];
+    for (int h = blockIdx.x; h < total; h += gridDim.x) {
+        const HeavyItem it = items[h];
+        const int i = it.row;
+        const long long kb = off[i] + static_cast<long long>(it.seg) * kHeavySegment;
+        const long long kend = min(off[i + 1], kb + kHeavySegment);
+        double vb = __longlong_as_double(0x7ff0000000000000ll);  // +inf: any neighbour beats it
+        int best = 0x7fffffff;
+        if (it.seg == 0) {  // the row itself is the initial candidate (ggd.cpp:15)
+            vb = __ldg(v + static_cast<long long>(i) * ld + s);
+            best = i;
+        }
+        long long k = kb + warp;
+        for (; k + (kHeavyUnroll - 1) * kWarps < kend; k += kHeavyUnroll * kWarps) {  // gathers in flight per warp
+            int j[kHeavyUnroll];
+            double vj[kHeavyUnroll];
+#pragma unroll
+            for (int u = 0; u < kHeavyUnroll; ++u) j[u] = __ldg(nbr + k + u * kWarps);
+#pragma unroll
+            for (int u = 0; u < kHeavyUnroll; ++u) vj[u] = __ldg(v + static_cast<long long>(j[u]) * ld + s);
+#pragma unroll
+            for (int u = 0; u < kHeavyUnroll; ++u)
+                if (lex_less(vj[u], j[u], vb, best)) {
+                    vb = vj[u];
+                    best = j[u];
+                }
+        }
+        for (; k < kend; k += kWarps) {
             const int j = __ldg(nbr + k);
             const double vj = __ldg(v + static_cast<long long>(j) * ld + s);
             if (lex_less(vj, j, vb, best)) {
@@ -651,9 +723,39 @@ __global__ void __launch_bounds__(kBlock) successors_heavy_kernel(const long lon
                     vb = sv[w][lane];
                     best = si[w][lane];
                 }
-            if (lane < Sc) O.out[static_cast<long long>(i - row_begin) * O.out_row + lane * O.out_col] = best;
+            if (it.slot < 0) {
+                if (lane < Sc) O.out[static_cast<long long>(i - row_begin) * O.out_row + lane * O.out_col] = best;
+            } else {
+                part_v[static_cast<long long>(it.slot) * 32 + lane] = vb;
+                part_i[static_cast<long long>(it.slot) * 32 + lane] = best;
+            }
         }
         __syncthreads();
+    }
+}
+
+// Successor of every multi-segment heavy row from its segments' partial minima
+// (warp per row, lane = sigma).
+__global__ void __launch_bounds__(kBlock) successors_combine_kernel(const HeavyRow* __restrict__ multi,
+                                                                    const int* __restrict__ counts,
+                                                                    const double* __restrict__ part_v,
+                                                                    const int* __restrict__ part_i, int Sc,
+                                                                    int row_begin, SuccOut O) {
+    const int lane = threadIdx.x & 31;
+    const int nrows = counts[2];
+    for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nrows; w += (gridDim.x * blockDim.x) >> 5) {
+        const HeavyRow r = multi[w];
+        double vb = part_v[static_cast<long long>(r.slot0) * 32 + lane];
+        int best = part_i[static_cast<long long>(r.slot0) * 32 + lane];
+        for (int q = 1; q < r.nseg; ++q) {
+            const double vq = part_v[static_cast<long long>(r.slot0 + q) * 32 + lane];
+            const int iq = part_i[static_cast<long long>(r.slot0 + q) * 32 + lane];
+            if (lex_less(vq, iq, vb, best)) {
+                vb = vq;
+                best = iq;
+            }
+        }
+        if (lane < Sc) O.out[static_cast<long long>(r.row - row_begin) * O.out_row + lane * O.out_col] = best;
     }
 }
 
@@ -851,10 +953,14 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
         e = cub::DeviceRadixSort::SortPairsDescending(temp, sort_bytes, deg_in, deg_out, id_in, id_out, rows, 0, 32, st);
         count_launch(2);
         if (e != cudaSuccess) return e;
-        // hub rows (see hub_split_kernel): longer than ~1/4096 of the entries
+        // hub rows (see hub_split_kernel): longer than ~1/4096 of the entries.
+        // The unit-weight fast-forward walks long rows with batched in-binade
+        // jumps (walk_events), so a hub costs it ~10^2 steps and no hub gets
+        // an SM of its own there.
         int* hub_count = counter + 1;
         int* hub_counter = counter + 2;
-        const long long threshold = std::max<long long>(4096, p.nnz / 4096);
+        const bool hubs = !(ff && p.weight_mode == kUnit);
+        const long long threshold = hubs ? std::max<long long>(4096, p.nnz / 4096) : (1ll << 62);
         hub_split_kernel<<<1, 1, 0, st>>>(deg_out, rows, threshold, hub_count, counter, hub_counter);
         count_launch();
         const RowSched R{id_out, counter, nullptr};
@@ -863,13 +969,18 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
         const dim3 wgrid(static_cast<unsigned>(
             std::min<long long>(want, static_cast<long long>(num_sms) * kWarpKernelBlocksPerSM)));
         SideStream& side = side_for(st);
-        cudaEventRecord(side.fork, st);
-        cudaStreamWaitEvent(side.stream, side.fork, 0);
+        if (hubs) {
+            cudaEventRecord(side.fork, st);
+            cudaStreamWaitEvent(side.stream, side.fork, 0);
+        }
         auto launch = [&](auto kernel) {
-            cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHubSmemBytes);
-            kernel<<<kMaxHubs, 32, kHubSmemBytes, side.stream>>>(p, T, Rh);  // first: hub blocks claim SMs
+            if (hubs) {
+                cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHubSmemBytes);
+                kernel<<<kMaxHubs, 32, kHubSmemBytes, side.stream>>>(p, T, Rh);  // first: hub blocks claim SMs
+                count_launch();
+            }
             kernel<<<wgrid, kBlock, 0, st>>>(p, T, R);
-            count_launch(2);
+            count_launch();
         };
         switch (p.weight_mode) {
             case kUnit:
@@ -885,8 +996,10 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
                 else launch(potential_warp_kernel<false, kEntryTable>);
                 break;
         }
-        cudaEventRecord(side.join, side.stream);
-        cudaStreamWaitEvent(st, side.join, 0);
+        if (hubs) {
+            cudaEventRecord(side.join, side.stream);
+            cudaStreamWaitEvent(st, side.join, 0);
+        }
         cudaFreeAsync(sched, st);
     } else {
         switch (p.weight_mode) {
@@ -912,20 +1025,33 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
 
 int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nbr, const double* v, int ld, int s0,
                       int n_sigma, int row_begin, int row_end, std::int32_t* out, long long out_row, long long out_col,
-                      void* pool, void* stream) {
+                      long long nnz, void* pool, void* stream) {
     (void)n;
     auto st = static_cast<cudaStream_t>(stream);
     auto off = reinterpret_cast<const long long*>(offsets);
     const int rows = row_end - row_begin;
     if (rows <= 0) return cudaSuccess;
+    // heavy rows have > kHeavyDegree entries each and multi-segment rows >
+    // kHeavySegment, so nnz bounds the items, partial slots and row lists
+    const long long heavy_max = std::min<long long>(rows, nnz / (kHeavyDegree + 1) + 1);
+    const long long seg_max = heavy_max + nnz / kHeavySegment + 1;
+    const long long multi_max = nnz / (kHeavySegment + 1) + 1;
+    const long long slot_max = 2 * multi_max + nnz / kHeavySegment + 1;
+    const std::size_t bytes_items = sizeof(HeavyItem) * seg_max, bytes_multi = sizeof(HeavyRow) * multi_max;
+    const std::size_t bytes_pv = sizeof(double) * 32 * slot_max, bytes_pi = sizeof(int) * 32 * slot_max;
+    const std::size_t head = 256;
     void* scratch = nullptr;
-    cudaError_t e = cudaMallocFromPoolAsync(&scratch, sizeof(int) * (static_cast<std::size_t>(rows) + 64),
+    cudaError_t e = cudaMallocFromPoolAsync(&scratch, head + bytes_pv + bytes_items + bytes_multi + bytes_pi,
                                             static_cast<cudaMemPool_t>(pool), st);
     if (e != cudaSuccess) return e;
-    int* count = static_cast<int*>(scratch);
-    int* list = count + 32;
-    cudaMemsetAsync(count, 0, sizeof(int), st);
-    mark_heavy_kernel<<<grid_for(rows), kBlock, 0, st>>>(off, row_begin, rows, list, count);
+    char* p = static_cast<char*>(scratch);
+    int* counts = reinterpret_cast<int*>(p);
+    double* part_v = reinterpret_cast<double*>(p + head);
+    auto* items = reinterpret_cast<HeavyItem*>(p + head + bytes_pv);
+    auto* multi = reinterpret_cast<HeavyRow*>(p + head + bytes_pv + bytes_items);
+    int* part_i = reinterpret_cast<int*>(p + head + bytes_pv + bytes_items + bytes_multi);
+    cudaMemsetAsync(counts, 0, 4 * sizeof(int), st);
+    mark_heavy_kernel<<<grid_for(rows), kBlock, 0, st>>>(off, row_begin, rows, items, counts, multi);
     count_launch(2);
     static int num_sms = 0;
     if (!num_sms) {
@@ -940,8 +1066,10 @@ int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nb
         const SuccOut O{out + c0 * out_col, out_row, out_col};
         const long long threads = static_cast<long long>(rows) * Sc;
         successors_kernel<<<grid_for(threads), kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, rows, O);
-        successors_heavy_kernel<<<num_sms * 8, kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, list, count, O);
-        count_launch(2);
+        successors_heavy_kernel<<<num_sms * 8, kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, items, counts,
+                                                                 part_v, part_i, O);
+        successors_combine_kernel<<<num_sms * 2, kBlock, 0, st>>>(multi, counts, part_v, part_i, Sc, row_begin, O);
+        count_launch(3);
     }
     cudaFreeAsync(scratch, st);
     return cudaGetLastError();

@@ -457,3 +457,51 @@ def test_batched_walk_hub_rows_bitwise(n):
         assert_bits(field[q], oracle_field(g, s, N.EXP_EIGEN))
     N.set_kernel(N.KERNEL_REPLAY)
     assert_bits(N.potentials(g.csr(N), sig), field)
+
+
+def test_multi_segment_hub_successors_and_labels():
+    # rows longer than one 2048-neighbour segment are reduced segment-wise and
+    # combined; successors / centers / labels must equal the oracle's
+    n = 9001
+    rng = np.random.default_rng(99)
+    u, v, _ = H.graphgen.random_edges(n, 3.0, unit=True, seed=99)
+    us, vs = [u], [v]
+    for h, deg in [(0, 2049), (n - 1, 8000), (4500, 4096), (17, 6000), (n // 3, 2100), (n // 5, 300)]:
+        nb = rng.choice(n, size=deg, replace=False)
+        nb = nb[nb != h]
+        us.append(np.full(len(nb), h, np.int32))
+        vs.append(nb.astype(np.int32))
+    g = H.G(n, np.concatenate(us), np.concatenate(vs), None, 10.0)
+    assert np.diff(g.offsets).max() > 3 * 2048
+    sig = [0.3, 1.0, 2.3, 5.0, 12.0, 30.0]
+    res, v_dev, succ = N.cluster_sweep(g.csr(N), sig, want_v=True, want_succ=True)
+    for q, s in enumerate(sig):
+        vo, so, co, cio, ko = O.cluster(g.offsets, g.nbr, g.wt, 10.0, s, workers=4)
+        assert_bits(v_dev[q], vo)
+        assert np.array_equal(succ[q], so)
+        assert np.array_equal(res[q].center, co) and np.array_equal(res[q].cluster_index, cio)
+        assert res[q].num_clusters == ko
+
+
+@pytest.mark.parametrize("kernel,unit,mode", [(N.KERNEL_FASTFWD, False, N.EXP_EIGEN),
+                                              (N.KERNEL_FASTFWD, False, N.EXP_GLIBC),
+                                              (N.KERNEL_REPLAY, True, N.EXP_EIGEN)])
+def test_hub_companion_launch_rows_bitwise(kernel, unit, mode):
+    # rows above max(4096, nnz/4096) entries run in the companion launch (own
+    # SM) for weighted graphs and the replay kernel; odd n puts the Eigen
+    # tail column next to the hub
+    setup(kernel, mode)
+    n = 8001
+    rng = np.random.default_rng(5)
+    u, v, w = H.graphgen.random_edges(n, 3.0, unit=unit, seed=5)
+    hub = rng.choice(n - 1, size=5000, replace=False) + 1
+    hub = np.append(hub[hub != n - 1], n - 1)
+    us = np.concatenate([u, np.zeros(len(hub), np.int32)])
+    vs = np.concatenate([v, hub.astype(np.int32)])
+    ws = None if unit else np.concatenate([w, 0.5 + 1.5 * rng.random(len(hub))])
+    g = H.G(n, us, vs, ws, 10.0)
+    assert np.diff(g.offsets).max() > 4096
+    sig = [0.7, 2.3, 9.0, 30.0] * 2  # 8 sigmas: the warp kernel
+    field = N.potentials(g.csr(N), sig)
+    for q, s in enumerate(sig[:4]):
+        assert_bits(field[q], oracle_field(g, s, mode))
