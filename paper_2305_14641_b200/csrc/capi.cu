@@ -124,7 +124,32 @@ struct DeviceCtx {
     cudaEvent_t slab_done[4] = {};
     cudaMemPool_t pool = nullptr;  // stream-ordered scratch that keeps its memory
     DevBuf off, nbr, w, v_nm, v_sm, succ, center, ci, nc, ws, tail, entry;
+    int* nc_host = nullptr;  // pinned staging for per-sigma counts (cudaHostAlloc)
+    int nc_host_cap = 0;
 };
+
+// Device->host copies into pageable memory block the calling thread until
+// they complete, which would stall the launches queued behind them.
+bool host_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+int* pinned_counts(DeviceCtx& C, int n) {
+    if (C.nc_host_cap < n) {
+        if (C.nc_host) cudaFreeHost(C.nc_host);
+        C.nc_host = nullptr;
+        C.nc_host_cap = 0;
+        cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&C.nc_host), sizeof(int) * n, cudaHostAllocDefault),
+                   "cudaHostAlloc");
+        C.nc_host_cap = n;
+    }
+    return C.nc_host;
+}
 
 DeviceCtx& ctx() {
     static std::map<int, DeviceCtx> all;
@@ -449,6 +474,13 @@ gqc_status gqc_resolve_centers(int32_t n, const int32_t* succ, int32_t* center, 
     });
 }
 
+#ifndef GQC_GGD_CHUNK
+#define GQC_GGD_CHUNK 16
+#endif
+// sigmas per GGD pass of the host pipeline: each pass's labels go down while
+// the next pass computes, so the last pass's download is the exposed tail
+constexpr int kGgdChunk = GQC_GGD_CHUNK;
+
 gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out,
                              int32_t* succ_out, int32_t* center_out, int32_t* cluster_index_out,
                              int32_t* num_clusters_out) {
@@ -515,15 +547,18 @@ gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_s
         }
         for (int k = 0; k < slabs; ++k) cuda_check(cudaStreamWaitEvent(st, C.slab_done[k], 0), "wait");
         tr.mark("potentials");
+        double* v_src = v_nm;
+        const bool v_early = v_out && host_pinned(v_out);  // pageable: copied after the GGD launches
         if (v_out) {  // sigma-major copy of the field
-            double* src = v_nm;
             if (n_sigma > 1) {
-                src = C.v_sm.get<double>(cells);
-                cuda_check(launch_transpose(v_nm, n, n_sigma, src, st), "transpose");
+                v_src = C.v_sm.get<double>(cells);
+                cuda_check(launch_transpose(v_nm, n, n_sigma, v_src, st), "transpose");
             }
-            cuda_check(cudaEventRecord(C.ev[8], st), "event");
-            cuda_check(cudaStreamWaitEvent(cs, C.ev[8], 0), "wait");
-            cuda_check(cudaMemcpyAsync(v_out, src, cells * sizeof(double), cudaMemcpyDeviceToHost, cs), "copy V");
+            if (v_early) {
+                cuda_check(cudaEventRecord(C.ev[8], st), "event");
+                cuda_check(cudaStreamWaitEvent(cs, C.ev[8], 0), "wait");
+                cuda_check(cudaMemcpyAsync(v_out, v_src, cells * sizeof(double), cudaMemcpyDeviceToHost, cs), "copy V");
+            }
         }
         int* ds = C.succ.get<int>(cells);
         int* dc = C.center.get<int>(cells);
@@ -531,33 +566,54 @@ gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_s
         int* dnc = C.nc.get<int>(n_sigma);
         const std::size_t wsb = labels_workspace_bytes(n, n_sigma);
         void* ws = C.ws.get<char>(wsb);
-        const int chunk = n_sigma > 16 ? 16 : n_sigma;
+        const int chunk = n_sigma > kGgdChunk ? kGgdChunk : n_sigma;
+        // labels of a chunk go down while the next chunk computes; into
+        // pageable buffers every copy blocks the host, so then all chunks are
+        // launched first and the copies queued after them
+        const bool overlap = host_pinned(cluster_index_out) && (!center_out || host_pinned(center_out)) &&
+                             (!succ_out || host_pinned(succ_out));
+        int* nc_stage = pinned_counts(C, n_sigma);
         int ev_i = 9;
-        for (int s0 = 0; s0 < n_sigma; s0 += chunk) {
-            const int Sc = std::min(chunk, n_sigma - s0);
+        auto download = [&](int s0, int Sc) {
             const std::size_t o = static_cast<std::size_t>(s0) * n, c = static_cast<std::size_t>(Sc) * n;
-            cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, s0, Sc, 0, n, ds + o, 1, n, nnz, C.pool, st), "successor kernel");
-            cuda_check(launch_chase(n, Sc, ds + o, dc + o, st), "chase kernel");
-            cuda_check(launch_labels(n, Sc, dc + o, dci + o, dnc + s0, ws, wsb, st), "label kernels");
-            tr.mark("ggd_chunk");
-            cudaEvent_t e = C.ev[ev_i];
-            ev_i = ev_i == 15 ? 9 : ev_i + 1;
-            cuda_check(cudaEventRecord(e, st), "event");
-            cuda_check(cudaStreamWaitEvent(cs, e, 0), "wait");
             if (succ_out)
                 cuda_check(cudaMemcpyAsync(succ_out + o, ds + o, c * sizeof(int), cudaMemcpyDeviceToHost, cs), "copy succ");
             if (center_out)
                 cuda_check(cudaMemcpyAsync(center_out + o, dc + o, c * sizeof(int), cudaMemcpyDeviceToHost, cs), "copy center");
             cuda_check(cudaMemcpyAsync(cluster_index_out + o, dci + o, c * sizeof(int), cudaMemcpyDeviceToHost, cs),
                        "copy cluster index");
-            cuda_check(cudaMemcpyAsync(num_clusters_out + s0, dnc + s0, Sc * sizeof(int), cudaMemcpyDeviceToHost, cs),
+            cuda_check(cudaMemcpyAsync(nc_stage + s0, dnc + s0, Sc * sizeof(int), cudaMemcpyDeviceToHost, cs),
                        "copy counts");
+        };
+        for (int s0 = 0; s0 < n_sigma; s0 += chunk) {
+            const int Sc = std::min(chunk, n_sigma - s0);
+            const std::size_t o = static_cast<std::size_t>(s0) * n;
+            cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, s0, Sc, 0, n, ds + o, 1, n, nnz, C.pool, st), "successor kernel");
+            cuda_check(launch_chase(n, Sc, ds + o, dc + o, st), "chase kernel");
+            cuda_check(launch_labels(n, Sc, dc + o, dci + o, dnc + s0, ws, wsb, st), "label kernels");
+            tr.mark("ggd_chunk");
+            if (overlap) {
+                cudaEvent_t e = C.ev[ev_i];
+                ev_i = ev_i == 15 ? 9 : ev_i + 1;
+                cuda_check(cudaEventRecord(e, st), "event");
+                cuda_check(cudaStreamWaitEvent(cs, e, 0), "wait");
+                download(s0, Sc);
+            }
         }
+        if (!overlap || (v_out && !v_early)) {
+            cuda_check(cudaEventRecord(C.ev[9], st), "event");
+            cuda_check(cudaStreamWaitEvent(cs, C.ev[9], 0), "wait");
+        }
+        if (!overlap)
+            for (int s0 = 0; s0 < n_sigma; s0 += chunk) download(s0, std::min(chunk, n_sigma - s0));
+        if (v_out && !v_early)
+            cuda_check(cudaMemcpyAsync(v_out, v_src, cells * sizeof(double), cudaMemcpyDeviceToHost, cs), "copy V");
         cuda_check(cudaEventRecord(C.ev[8], cs), "event");
         cuda_check(cudaStreamWaitEvent(st, C.ev[8], 0), "wait");
         tr.mark("downloads");
         cuda_check(cudaStreamSynchronize(cs), "cluster sweep (copies)");
         cuda_check(cudaStreamSynchronize(st), "cluster sweep");
+        std::copy(nc_stage, nc_stage + n_sigma, num_clusters_out);
     });
 }
 
