@@ -78,6 +78,13 @@ gqc_status gqc_set_option(gqc_option key, int64_t value);
 gqc_status gqc_get_option(gqc_option key, int64_t* value);
 /* Number of CUDA devices visible (0 on a machine without a GPU). */
 int32_t gqc_device_count(void);
+/* Optional: create the current device's context, streams and memory pool and
+ * load the sweep kernels now (every entry point otherwise does this on first
+ * use). Safe to call from a helper thread while the caller parses its input,
+ * as long as no other gqc_* call runs concurrently. No reference counterpart
+ * (the reference has no device); the CLI uses it to overlap CUDA start-up
+ * (~0.5-1.5 s per process) with edge-list parsing. */
+gqc_status gqc_init(void);
 
 /* ---------------------------------------------------------------- host API */
 

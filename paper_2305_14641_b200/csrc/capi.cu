@@ -151,7 +151,7 @@ int* pinned_counts(DeviceCtx& C, int n) {
     return C.nc_host;
 }
 
-DeviceCtx& ctx() {
+DeviceCtx& ctx() {  // callers hold g_mu (guarded)
     static std::map<int, DeviceCtx> all;
     int dev = 0;
     int count = 0;
@@ -368,6 +368,26 @@ int32_t gqc_device_count(void) {
     return c;
 }
 
+static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out,
+                               int32_t* succ_out, int32_t* center_out, int32_t* cluster_index_out,
+                               int32_t* num_clusters_out);
+
+gqc_status gqc_init(void) {
+    return guarded([&] {
+        ctx();
+        // one tiny sweep on the warp-per-row path (8 sigmas) and on the
+        // thread-per-row path (1 sigma): creates the context's streams and
+        // pool and loads the modules of the kernels a sweep launches
+        const std::int64_t off[4] = {0, 1, 3, 4};
+        const std::int32_t nbr[4] = {1, 0, 2, 1};
+        const gqc_csr g{3, 4, off, nbr, nullptr, 10.0};
+        double sig[8];
+        for (int k = 0; k < 8; ++k) sig[k] = 1.0 + k;
+        std::int32_t ci[24], nc[8];
+        for (int S : {8, 1}) cluster_sweep_impl(&g, sig, S, nullptr, nullptr, nullptr, ci, nc);
+    });
+}
+
 gqc_status gqc_set_option(gqc_option key, int64_t value) {
     return guarded([&] {
         if (key == GQC_OPT_EXP_MODE) {
@@ -481,10 +501,10 @@ gqc_status gqc_resolve_centers(int32_t n, const int32_t* succ, int32_t* center, 
 // the next pass computes, so the last pass's download is the exposed tail
 constexpr int kGgdChunk = GQC_GGD_CHUNK;
 
-gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out,
-                             int32_t* succ_out, int32_t* center_out, int32_t* cluster_index_out,
-                             int32_t* num_clusters_out) {
-    return guarded([&] {
+// The body of gqc_cluster_sweep (callers hold g_mu).
+static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out, int32_t* succ_out,
+                        int32_t* center_out, int32_t* cluster_index_out, int32_t* num_clusters_out) {
+    {
         check_sigmas(sigmas, n_sigma);
         check_csr_shape(g);
         if (!cluster_index_out || !num_clusters_out) fail(GQC_EINVAL, "null output");
@@ -614,6 +634,14 @@ gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_s
         cuda_check(cudaStreamSynchronize(cs), "cluster sweep (copies)");
         cuda_check(cudaStreamSynchronize(st), "cluster sweep");
         std::copy(nc_stage, nc_stage + n_sigma, num_clusters_out);
+    }
+}
+
+gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out,
+                             int32_t* succ_out, int32_t* center_out, int32_t* cluster_index_out,
+                             int32_t* num_clusters_out) {
+    return guarded([&] {
+        cluster_sweep_impl(g, sigmas, n_sigma, v_out, succ_out, center_out, cluster_index_out, num_clusters_out);
     });
 }
 

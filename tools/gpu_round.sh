@@ -13,3 +13,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
     python bench.py --profile --steps 1 --warmup 1 > gpurun_out/ncu_launches.log 2>&1; echo "ncu_launches=$?"
 ncu --set full --clock-control none --import-source on -k regex:"potential_warp|successors_kernel" -s 2 -c 2 \
     -o gpurun_out/prof_full python bench.py --profile --steps 1 --warmup 1 > gpurun_out/ncu_full.log 2>&1; echo "ncu_full=$?"
+python bench.py --workload sbm100k > gpurun_out/bench_sbm.json 2> gpurun_out/bench_sbm.err; echo "bench_sbm=$?"
+python bench.py --workload rmat22 --steps 10 > gpurun_out/bench_rmat.json 2> gpurun_out/bench_rmat.err; echo "bench_rmat=$?"
+timeout 900 python tools/e2e_qc.py > gpurun_out/e2e_qc.json 2> gpurun_out/e2e_qc.err; echo "e2e_qc=$?"
