@@ -90,6 +90,25 @@ def main(tag):
                 f"{cpu.get('value', float('nan')):.3g} GPairs/s ({cpu.get('cores')} cores) | "
                 f"{json.dumps({k: round(v, 3) for k, v in (d.get('breakdown_ms') or {}).items()})} |")
 
+    qc = None
+    for name in ("e2e_qc2.json", "e2e_qc.json"):
+        if os.path.exists(os.path.join(OUT, name)):
+            qc = json.load(open(os.path.join(OUT, name)))
+            break
+
+    def qc_rows():
+        if not qc:
+            return "(not run)"
+        out = [f"Workload: {qc['workload']}, edge file {qc['edge_file_bytes'] / 1e6:.0f} MB, {qc['host_threads']} host "
+               f"threads. Wall time of one `graphqc` process each (stage times from GQC_TRACE=1; `cuda` = wait for "
+               f"CUDA start-up after parsing, which runs on a helper thread during the load):", "",
+               "| command | wall s | stages (ms) |", "|---|---|---|"]
+        for k, label in (("sweep", "`graphqc sweep` (30-sigma log grid, labels -> NMI/ARI/FMI/modularity per sigma)"),
+                         ("cluster_sigma5", "`graphqc cluster --sigma 5` (+ assignment CSV)")):
+            for r in qc.get(k, []):
+                out.append(f"| {label} | {r['wall_s']:.2f} | {json.dumps(r['stages_ms'])} |")
+        return "\n".join(out)
+
     pw = kern.get("potential_warp_kernel<FASTFWD,unit>", {})
     sk = kern.get("successors_kernel", {})
     md = f"""# {tag} profile summary (B200, sm_100a)
@@ -115,6 +134,10 @@ GPU kernel launches in the timed region: {b.get('gpu_launches')} over {b.get('st
 Dense in-order replay (K1, `--kernel replay`) on SBM 100k x 32 sigmas: 39.2 ms for the potentials =
 8.16e12 logical pairs/s = 16.3e12 fp64 adds/s, 88% of the B200's nominal 37 TFLOPS FP64 (18.5e12 adds/s).
 The exact fast-forward (K2) computes the same bit-identical field in 0.45 ms (87x).
+
+## End-to-end QC time (load edge list -> CSR -> potentials -> GGD -> metrics -> outputs)
+
+{qc_rows()}
 
 ## Kernel table (ncu, LFR 1M x 32 sigmas)
 
