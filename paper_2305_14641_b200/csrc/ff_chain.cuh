@@ -227,6 +227,46 @@ GQC_HD inline void ff_run2(Chain& a, const double ca, Chain& b, const double cb,
     if (Lb > 0) ff_run(b, cb, Lb);
 }
 
+// One step of a W run for ff_walk2: either the whole remainder inside the
+// binade (returns with L = 0), or the maximal in-binade jump plus the crossing
+// add and an incremental refresh (settled chains), or one real add (c >=
+// base/2, or the odd side of a half-ulp tie). Every branch consumes >= 1 add.
+GQC_HD inline void ff_step(Chain& ch, const double c, int& L) {
+    const bool ok = settled(ch);
+    const double t = gqc_fma(static_cast<double>(L), ch.inc, ch.s);
+    if (ok && t < ch.top) {
+        ch.s = t;
+        L = 0;
+        return;
+    }
+    if (ok) {
+        const double m = max_steps(ch, room_of(ch));
+        const double top = ch.top;
+        ch.s = gqc_add(gqc_fma(m, ch.inc, ch.s), c);
+        L -= static_cast<int>(m) + 1;
+        ch.top = gqc_add(top, top);  // landed in [top, 2 top): see ff_pass
+        ch.inc = gqc_sub(gqc_add(top, c), top);
+        ch.flags = kJump | (exp_field(top) == ch.f_tie ? kTie : 0);
+    } else {
+        ch.s = gqc_add(ch.s, c);
+        --L;
+        refresh(ch, c);
+    }
+}
+
+// Both chains of a W run of length L > 0 in one loop: the warp iterates
+// 1 + (most binade crossings of any lane and chain) times over one compact
+// body instead of a pass per chain plus the general loop for multi-crossings.
+GQC_HD inline void ff_walk2(Chain& a, const double ca, Chain& b, const double cb, const int L) {
+    if (!(a.s < a.top)) refresh(a, ca);
+    if (!(b.s < b.top)) refresh(b, cb);
+    int La = L, Lb = L;
+    do {
+        if (La > 0) ff_step(a, ca, La);
+        if (Lb > 0) ff_step(b, cb, Lb);
+    } while (La > 0 || Lb > 0);
+}
+
 // ---------------------------------------------------------------------------
 // Batched walk over neighbour events (unit weights). Event q of a chunk is the
 // run of W terms over columns [pos, col(q)) followed by one neighbour term c1

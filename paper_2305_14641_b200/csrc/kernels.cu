@@ -27,6 +27,9 @@
 #ifndef GQC_CONST_SMEM
 #define GQC_CONST_SMEM 1
 #endif
+#ifndef GQC_WALK2
+#define GQC_WALK2 1
+#endif
 #ifndef GQC_LANE_OUT_SMEM
 #define GQC_LANE_OUT_SMEM 1
 #endif
@@ -397,7 +400,11 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
                     ch.top = 0.0;
                 }
             } else {
+#if GQC_WALK2
+                ff_walk2(num, pW, den, eW, L);
+#else
                 ff_run2(num, pW, den, eW, L);
+#endif
             }
         } else {
             replay(num.s, den.s, pW, eW, L);

@@ -241,6 +241,71 @@ long long fft_rows2(std::uint64_t seed, int nrows, int ncols, double* bad) {
     return mism;
 }
 
+// fft_rows2 with the single-loop two-chain walk (ff_walk2).
+long long fft_rows2w(std::uint64_t seed, int nrows, int ncols, double* bad) {
+    Rng r{seed};
+    long long mism = 0;
+    int tp[2][kPrefixCap];
+    double sp[2][kPrefixCap], ip[2][kPrefixCap];
+    for (int row = 0; row < nrows; ++row) {
+        const int ew = 1 + r.below(1060);
+        const double e = rand_double(r, ew, ew);
+        const double p = 100.0 * e;
+        const double te = rand_double(r, ew + r.below(40), ew + 40);
+        const double tpv = 1.0 * te;
+        int cnt[2], tend[2];
+        double send[2];
+        build_prefix(p, ncols, tp[0], sp[0], ip[0], &cnt[0], &tend[0], &send[0]);
+        build_prefix(e, ncols, tp[1], sp[1], ip[1], &cnt[1], &tend[1], &send[1]);
+        const int deg = 1 + r.below(40);
+        const int self = r.below(ncols);
+        Chain num = make_chain(0.0, p), den = make_chain(0.0, e);
+        double rn = 0.0, rd = 0.0;
+        int pos = 0;
+        bool first = true;
+        for (int q = 0; q <= deg; ++q) {
+            int col = q == deg ? ncols : pos + r.below((ncols - pos) / (deg - q + 1) * 2 + 1);
+            if (col > ncols) col = ncols;
+            const int L = col - pos;
+            if (L > 0) {
+                if (first) {
+                    if (L < tend[0]) num.s = prefix_value(tp[0], sp[0], ip[0], cnt[0], L);
+                    else { num.s = send[0]; ff_run(num, p, L - tend[0]); }
+                    if (L < tend[1]) den.s = prefix_value(tp[1], sp[1], ip[1], cnt[1], L);
+                    else { den.s = send[1]; ff_run(den, e, L - tend[1]); }
+                    num.top = 0.0;
+                    den.top = 0.0;
+                } else {
+                    ff_walk2(num, p, den, e, L);
+                }
+                rn = naive(rn, p, L);
+                rd = naive(rd, e, L);
+            }
+            first = false;
+            if (col >= ncols) break;
+            if (col == self) {
+                den.s = den.s + 1.0;
+                rd = rd + 1.0;
+            } else {
+                num.s = num.s + tpv;
+                den.s = den.s + te;
+                rn = rn + tpv;
+                rd = rd + te;
+            }
+            pos = col + 1;
+        }
+        if (std::memcmp(&num.s, &rn, sizeof rn) != 0 || std::memcmp(&den.s, &rd, sizeof rd) != 0) {
+            if (mism == 0 && bad) {
+                bad[0] = e;
+                bad[1] = te;
+                bad[2] = row;
+            }
+            ++mism;
+        }
+    }
+    return mism;
+}
+
 double fft_run(double s, double c, int L) {
     Chain ch = make_chain(s, c);
     ff_run(ch, c, L);

@@ -70,9 +70,14 @@ def test_prefix_segments_bitwise(ff, seed):
 
 
 @pytest.mark.parametrize("seed", [31, 32])
-def test_two_chain_rows_with_prefix_bitwise(ff, seed):
+@pytest.mark.parametrize("walk", ["fft_rows2", "fft_rows2w"])
+def test_two_chain_rows_with_prefix_bitwise(ff, seed, walk):
+    # ff_run2 (pass per chain + general loop) and ff_walk2 (one loop, both chains)
+    fn = getattr(ff, walk)
+    fn.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_void_p]
+    fn.restype = C.c_longlong
     bad = np.zeros(3)
-    m = ff.fft_rows2(seed, 3000, 20000, bad.ctypes.data_as(C.c_void_p))
+    m = fn(seed, 3000, 20000, bad.ctypes.data_as(C.c_void_p))
     assert m == 0, f"{m} mismatches, first (e, term, row) = {bad.tolist()}"
 
 
