@@ -609,8 +609,8 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
             const int Sc = std::min(chunk, n_sigma - s0);
             const std::size_t o = static_cast<std::size_t>(s0) * n;
             cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, s0, Sc, 0, n, ds + o, 1, n, nnz, C.pool, st), "successor kernel");
-            cuda_check(launch_chase(n, Sc, ds + o, dc + o, st), "chase kernel");
-            cuda_check(launch_labels(n, Sc, dc + o, dci + o, dnc + s0, ws, wsb, st), "label kernels");
+            cuda_check(launch_chase(n, Sc, ds + o, dc + o, st, ws), "chase kernel");
+            cuda_check(launch_labels(n, Sc, dc + o, dci + o, dnc + s0, ws, wsb, st, true), "label kernels");
             tr.mark("ggd_chunk");
             if (overlap) {
                 cudaEvent_t e = C.ev[ev_i];
@@ -692,8 +692,8 @@ gqc_status gqc_dev_ggd(const gqc_csr* g, const double* v, int32_t n_sigma, int32
         DeviceCtx& C = ctx();
         int* s = succ ? succ : center;  // the chase runs in place on center
         cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, 0, g->n, s, 1, g->n, g->nnz, C.pool, st), "successor kernel");
-        cuda_check(launch_chase(g->n, n_sigma, s, center, st), "chase kernel");
-        cuda_check(launch_labels(g->n, n_sigma, center, cluster_index, num_clusters, workspace, workspace_bytes, st),
+        cuda_check(launch_chase(g->n, n_sigma, s, center, st, workspace), "chase kernel");
+        cuda_check(launch_labels(g->n, n_sigma, center, cluster_index, num_clusters, workspace, workspace_bytes, st, true),
                    "label kernels");
     });
 }
@@ -725,8 +725,8 @@ gqc_status gqc_dev_resolve(int32_t n, int32_t n_sigma, const int32_t* succ_nm, i
         if (workspace_bytes < labels_workspace_bytes(n, n_sigma)) fail(GQC_EINVAL, "workspace too small");
         auto st = static_cast<cudaStream_t>(stream);
         cuda_check(launch_transpose_i32(succ_nm, n, n_sigma, center, st), "transpose");
-        cuda_check(launch_chase(n, n_sigma, center, center, st), "chase kernel");
-        cuda_check(launch_labels(n, n_sigma, center, cluster_index, num_clusters, workspace, workspace_bytes, st),
+        cuda_check(launch_chase(n, n_sigma, center, center, st, workspace), "chase kernel");
+        cuda_check(launch_labels(n, n_sigma, center, cluster_index, num_clusters, workspace, workspace_bytes, st, true),
                    "label kernels");
     });
 }

@@ -267,7 +267,6 @@ GQC_HD inline void ff_walk2(Chain& a, const double ca, Chain& b, const double cb
         if (La > 0) ff_step(a, ca, La);
         if (Lb > 0) ff_step(b, cb, Lb);
     } while (La > 0 || Lb > 0);
-
 }
 
 // ---------------------------------------------------------------------------

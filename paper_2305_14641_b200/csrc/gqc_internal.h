@@ -67,10 +67,13 @@ int launch_successors(std::int32_t n, const std::int64_t* offsets, const std::in
                       std::int32_t row_end, std::int32_t* out, long long out_row, long long out_col, long long nnz,
                       void* pool, void* stream);
 int launch_transpose_i32(const std::int32_t* in, std::int32_t n, std::int32_t n_sigma, std::int32_t* out, void* stream);
+// labels_workspace (optional): launch_labels' workspace; the chase then writes
+// the center flags there and launch_labels must be called with flags_ready.
 int launch_chase(std::int32_t n, std::int32_t n_sigma, const std::int32_t* succ_sm, std::int32_t* center_sm,
-                 void* stream);
+                 void* stream, void* labels_workspace = nullptr);
 int launch_labels(std::int32_t n, std::int32_t n_sigma, const std::int32_t* center_sm, std::int32_t* cluster_index_sm,
-                  std::int32_t* num_clusters, void* workspace, std::size_t ws_bytes, void* stream);
+                  std::int32_t* num_clusters, void* workspace, std::size_t ws_bytes, void* stream,
+                  bool flags_ready = false);
 std::size_t labels_workspace_bytes(std::int32_t n, std::int32_t n_sigma);
 int launch_transpose(const double* v_nm, std::int32_t n, std::int32_t n_sigma, double* v_sm, void* stream);
 // Checked resolve for arbitrary successor maps: writes center/cluster_index,

@@ -596,17 +596,20 @@ __global__ void __launch_bounds__(kBlock) successors_kernel(const long long* __r
                                                             const int* __restrict__ nbr,
                                                             const double* __restrict__ v, int ld, int s0, int Sc,
                                                             int row_begin, int rows, SuccOut O) {
-    const long long tid = static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x;
-    const int q = static_cast<int>(tid % Sc);
-    const long long r = tid / Sc;
-    if (r >= rows) return;
+    // rows * Sc < 2^31 (launch_successors checks): 32-bit index math
+    const unsigned tid = blockIdx.x * static_cast<unsigned>(kBlock) + threadIdx.x;
+    const unsigned r = tid / static_cast<unsigned>(Sc);
+    const int q = static_cast<int>(tid - r * static_cast<unsigned>(Sc));
+    if (r >= static_cast<unsigned>(rows)) return;
     const int s = s0 + q;
     const int i = row_begin + static_cast<int>(r);
-    const long long kend = off[i + 1];
-    if (kend - off[i] > kHeavyDegree) return;  // heavy rows: successors_heavy_kernel
-    int best = i;
+    // the row's own potential is loaded alongside its offsets (independent
+    // loads in flight together; an isolated row keeps best = i)
     double vb = __ldg(v + static_cast<long long>(i) * ld + s);
     long long k = off[i];
+    const long long kend = off[i + 1];
+    if (kend - k > kHeavyDegree) return;  // heavy rows: successors_heavy_kernel
+    int best = i;
     // kSuccUnroll independent gathers in flight, compared in ascending k
     for (; k + kSuccUnroll <= kend; k += kSuccUnroll) {
         int j[kSuccUnroll];
@@ -630,7 +633,7 @@ __global__ void __launch_bounds__(kBlock) successors_kernel(const long long* __r
             vb = vj;
         }
     }
-    O.out[r * O.out_row + q * O.out_col] = best;
+    O.out[static_cast<long long>(r) * O.out_row + q * O.out_col] = best;
 }
 
 // Heavy rows (degree > kHeavyDegree, e.g. R-MAT hubs with ~10^5 neighbours)
@@ -787,10 +790,13 @@ __global__ void transpose_i32_kernel(const int* __restrict__ in, int n, int S, i
 // overwrite with roots as they finish (any value read is an ancestor, so the
 // result is exact; finished neighbours shorten the walk). Maps built by K3
 // strictly decrease (v, id) along a chain, so every walk terminates.
-__global__ void __launch_bounds__(kBlock) chase_kernel(int n, int* __restrict__ center) {
+// With flag != nullptr it also writes the center flags of K5a (flag[b + i] =
+// root == i), saving the label pass its read of center[].
+__global__ void __launch_bounds__(kBlock) chase_kernel(int n, int* __restrict__ center, int* __restrict__ flag) {
     const int i = blockIdx.x * kBlock + threadIdx.x;
     if (i >= n) return;
-    int* c = center + static_cast<long long>(blockIdx.y) * n;
+    const long long b = static_cast<long long>(blockIdx.y) * n;
+    int* c = center + b;
     int x = c[i];
     for (;;) {
         const int y = c[x];
@@ -798,6 +804,7 @@ __global__ void __launch_bounds__(kBlock) chase_kernel(int n, int* __restrict__ 
         x = y;
     }
     c[i] = x;
+    if (flag) flag[b + i] = x == i ? 1 : 0;
 }
 
 // K5a: center flags for the dense relabel scan (flag[S*n] = 0 terminator).
@@ -1072,6 +1079,7 @@ int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nb
         const int Sc = std::min(32, n_sigma - c0);
         const SuccOut O{out + c0 * out_col, out_row, out_col};
         const long long threads = static_cast<long long>(rows) * Sc;
+        if (threads >= (1ll << 31) - kBlock) return cudaErrorInvalidValue;  // 32-bit thread ids
         successors_kernel<<<grid_for(threads), kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, rows, O);
         successors_heavy_kernel<<<num_sms * 8, kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, items, counts,
                                                                  part_v, part_i, O);
@@ -1089,14 +1097,20 @@ int launch_transpose_i32(const std::int32_t* in, int n, int n_sigma, std::int32_
     return cudaGetLastError();
 }
 
-int launch_chase(int n, int n_sigma, const std::int32_t* succ_sm, std::int32_t* center_sm, void* stream) {
+int launch_chase(int n, int n_sigma, const std::int32_t* succ_sm, std::int32_t* center_sm, void* stream,
+                 void* labels_workspace) {
     auto st = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaSuccess;
     if (succ_sm != center_sm)
         e = cudaMemcpyAsync(center_sm, succ_sm, sizeof(int) * static_cast<size_t>(n) * n_sigma,
                             cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return e;
-    chase_kernel<<<dim3(grid_for(n), n_sigma), kBlock, 0, st>>>(n, center_sm);
+    int* flag = static_cast<int*>(labels_workspace);  // launch_labels' flag array (first in its workspace)
+    if (flag) {
+        e = cudaMemsetAsync(flag + static_cast<long long>(n) * n_sigma, 0, sizeof(int), st);  // scan terminator
+        if (e != cudaSuccess) return e;
+    }
+    chase_kernel<<<dim3(grid_for(n), n_sigma), kBlock, 0, st>>>(n, center_sm, flag);
     count_launch();
     return cudaGetLastError();
 }
@@ -1111,7 +1125,7 @@ std::size_t labels_workspace_bytes(int n, int n_sigma) {
 }
 
 int launch_labels(int n, int n_sigma, const std::int32_t* center_sm, std::int32_t* ci_sm, std::int32_t* num_clusters,
-                  void* workspace, std::size_t ws_bytes, void* stream) {
+                  void* workspace, std::size_t ws_bytes, void* stream, bool flags_ready) {
     auto st = static_cast<cudaStream_t>(stream);
     const long long items = static_cast<long long>(n) * n_sigma + 1;
     auto align = [](std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); };
@@ -1120,8 +1134,10 @@ int launch_labels(int n, int n_sigma, const std::int32_t* center_sm, std::int32_
     int* scan = reinterpret_cast<int*>(w + align(sizeof(int) * items));
     void* temp = w + 2 * align(sizeof(int) * items);
     std::size_t temp_bytes = ws_bytes - 2 * align(sizeof(int) * items);
-    center_flags_kernel<<<grid_for(items), kBlock, 0, st>>>(n, n_sigma, center_sm, flag);
-    count_launch();
+    if (!flags_ready) {  // else launch_chase wrote them
+        center_flags_kernel<<<grid_for(items), kBlock, 0, st>>>(n, n_sigma, center_sm, flag);
+        count_launch();
+    }
     cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, flag, scan, items, st);
     count_launch(2);  // CUB: init + scan kernels
     if (e != cudaSuccess) return e;
