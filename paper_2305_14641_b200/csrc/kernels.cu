@@ -339,6 +339,9 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
     __shared__ int pt[kFF ? 2 * kMaxSigmaPerLaunch * kPrefixStride : 1];
     __shared__ int pcount[2 * kMaxSigmaPerLaunch], pend[2 * kMaxSigmaPerLaunch];
     __shared__ int batch_cols[(kFF && kW == kUnit) ? kBlock : 1];  // per-warp neighbour chunk (batched rows)
+    // pstart[q][e]: last prefix segment of chain q whose start t <= 2^e (the
+    // segments double in length, so a lookup plus a step or two finds a run's)
+    __shared__ unsigned char pstart[kFF ? 2 * kMaxSigmaPerLaunch : 1][32];
     const int S = P.n_sigma;
     for (int idx = threadIdx.x; idx < kSigmaFields * kMaxSigmaPerLaunch; idx += blockDim.x) {
         const int ss = idx % kMaxSigmaPerLaunch, f = idx / kMaxSigmaPerLaunch;
@@ -352,6 +355,14 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
         for (int q = threadIdx.x; q < 2 * S; q += blockDim.x) {
             pcount[q] = T.count[q];
             pend[q] = T.t_end[q];
+        }
+        for (int idx = threadIdx.x; idx < 2 * S * 32; idx += blockDim.x) {
+            const int q = idx >> 5, e = idx & 31;
+            const long long lim = 1ll << e;
+            int k = 0;
+            const int cnt = T.count[q];
+            while (k + 1 < cnt && T.t[q * kPrefixCap + k + 1] <= lim) ++k;
+            pstart[q][e] = static_cast<unsigned char>(k);
         }
     }
     __syncthreads();
@@ -385,12 +396,9 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
                     Chain& ch = c ? den : num;
                     if (L < pend[q]) {
                         const int* tq = pt + q * kPrefixStride;
-                        int lo = 0, hi = pcount[q] - 1;
-                        while (lo < hi) {
-                            const int mid = (lo + hi + 1) >> 1;
-                            if (tq[mid] <= L) lo = mid;
-                            else hi = mid - 1;
-                        }
+                        int lo = pstart[q][31 - __clz(L)];  // t[lo] <= 2^floor(log2 L) <= L
+                        const int last = pcount[q] - 1;
+                        while (lo < last && tq[lo + 1] <= L) ++lo;
                         ch.s = __fma_rn(static_cast<double>(L - tq[lo]), T.inc[q * kPrefixCap + lo],
                                         T.s0[q * kPrefixCap + lo]);
                     } else {
