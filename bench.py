@@ -239,6 +239,7 @@ def run_native(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     N.set_kernel(N.KERNEL_FASTFWD if args.kernel == "fastfwd" else N.KERNEL_REPLAY)
+    N.set_device(local)  # libgqc's own CUDA runtime: host-API calls on this rank's GPU
 
     off, nbr, desc = make_graph(args.workload)
     n, nnz = len(off) - 1, len(nbr)

@@ -70,7 +70,12 @@ typedef enum gqc_exp_mode { GQC_EXP_EIGEN = 0, GQC_EXP_GLIBC = 1 } gqc_exp_mode;
  * Both are bit-identical to the reference's ascending-j fp64 sums. */
 typedef enum gqc_kernel { GQC_KERNEL_FASTFWD = 0, GQC_KERNEL_REPLAY = 1 } gqc_kernel;
 
-typedef enum gqc_option { GQC_OPT_EXP_MODE = 1, GQC_OPT_KERNEL = 2 } gqc_option;
+/* GQC_OPT_DEVICE: CUDA device ordinal of the host-buffer entry points
+ * (default 0). The gqc_dev_* entry points run on the device of the stream
+ * they are given (or, for the legacy default stream, of their buffers):
+ * libgqc links its own CUDA runtime, so the caller's current device does not
+ * carry over. */
+typedef enum gqc_option { GQC_OPT_EXP_MODE = 1, GQC_OPT_KERNEL = 2, GQC_OPT_DEVICE = 3 } gqc_option;
 
 const char* gqc_last_error(void);
 const char* gqc_version(void);

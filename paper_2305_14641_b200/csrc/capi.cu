@@ -31,6 +31,7 @@ std::mutex g_mu;  // calls are serialized per process
 struct Options {
     int exp_mode = GQC_EXP_EIGEN;
     int kernel = GQC_KERNEL_FASTFWD;
+    int device = 0;  // device of the host-buffer entry points (GQC_OPT_DEVICE)
 } g_opt;
 
 struct Fail {
@@ -151,7 +152,24 @@ int* pinned_counts(DeviceCtx& C, int n) {
     return C.nc_host;
 }
 
-DeviceCtx& ctx() {  // callers hold g_mu (guarded)
+// libgqc carries its own (static) CUDA runtime, whose current device is not
+// the caller's (torch.cuda.set_device does not reach it). Every call binds it
+// explicitly: device-resident entry points to the device of the caller's
+// stream (or of a buffer when the stream is the legacy default), host-buffer
+// entry points to GQC_OPT_DEVICE.
+void bind_device(cudaStream_t st, const void* dptr) {
+    int dev = g_opt.device;
+    if (st) {
+        cuda_check(cudaStreamGetDevice(st, &dev), "cudaStreamGetDevice");
+    } else if (dptr) {
+        cudaPointerAttributes a{};
+        cuda_check(cudaPointerGetAttributes(&a, dptr), "cudaPointerGetAttributes");
+        if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) dev = a.device;
+    }
+    cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+}
+
+DeviceCtx& ctx(cudaStream_t st = nullptr, const void* dptr = nullptr) {  // callers hold g_mu (guarded)
     static std::map<int, DeviceCtx> all;
     int dev = 0;
     int count = 0;
@@ -159,6 +177,7 @@ DeviceCtx& ctx() {  // callers hold g_mu (guarded)
         cudaGetLastError();
         fail(GQC_ECUDA, "no CUDA device available (libgqc has no CPU path)");
     }
+    bind_device(st, dptr);
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     DeviceCtx& c = all[dev];
     if (!c.stream) {
@@ -396,6 +415,14 @@ gqc_status gqc_set_option(gqc_option key, int64_t value) {
         } else if (key == GQC_OPT_KERNEL) {
             if (value != GQC_KERNEL_FASTFWD && value != GQC_KERNEL_REPLAY) fail(GQC_EINVAL, "unknown kernel");
             g_opt.kernel = static_cast<int>(value);
+        } else if (key == GQC_OPT_DEVICE) {
+            int count = 0;
+            if (cudaGetDeviceCount(&count) != cudaSuccess) {
+                cudaGetLastError();
+                count = 0;
+            }
+            if (value < 0 || value >= count) fail(GQC_EINVAL, "device ordinal out of range");
+            g_opt.device = static_cast<int>(value);
         } else {
             fail(GQC_EINVAL, "unknown option");
         }
@@ -407,6 +434,7 @@ gqc_status gqc_get_option(gqc_option key, int64_t* value) {
         if (!value) fail(GQC_EINVAL, "null output");
         if (key == GQC_OPT_EXP_MODE) *value = g_opt.exp_mode;
         else if (key == GQC_OPT_KERNEL) *value = g_opt.kernel;
+        else if (key == GQC_OPT_DEVICE) *value = g_opt.device;
         else fail(GQC_EINVAL, "unknown option");
     });
 }
@@ -652,7 +680,7 @@ gqc_status gqc_dev_potentials(const gqc_csr* g, const double* sigmas, int32_t n_
         check_csr_shape(g);
         if (row_begin < 0 || row_end > g->n || row_begin > row_end) fail(GQC_ERANGE, "row range out of range");
         if (!v_rows && row_end > row_begin) fail(GQC_EINVAL, "null output");
-        DeviceCtx& C = ctx();
+        DeviceCtx& C = ctx(static_cast<cudaStream_t>(stream), g->offsets);
         run_potentials(C, *g, sigmas, n_sigma, row_begin, row_end, v_rows, nullptr, static_cast<cudaStream_t>(stream));
     });
 }
@@ -669,7 +697,7 @@ gqc_status gqc_dev_potentials_packed(const gqc_csr* g, const double* sigmas, int
         const int chunks = (n_sigma + chunk - 1) / chunk;
         if (chunks > 1 && chunk_stride < static_cast<int64_t>(row_end - row_begin) * chunk)
             fail(GQC_EINVAL, "chunk stride smaller than one chunk");
-        DeviceCtx& C = ctx();
+        DeviceCtx& C = ctx(static_cast<cudaStream_t>(stream), g->offsets);
         run_potentials(C, *g, sigmas, n_sigma, row_begin, row_end, v_out, nullptr, static_cast<cudaStream_t>(stream),
                        nullptr, chunk, chunk_stride);
     });
@@ -689,7 +717,7 @@ gqc_status gqc_dev_ggd(const gqc_csr* g, const double* v, int32_t n_sigma, int32
         if (!v || !center || !cluster_index || !num_clusters || !workspace) fail(GQC_EINVAL, "null buffer");
         if (workspace_bytes < labels_workspace_bytes(g->n, n_sigma)) fail(GQC_EINVAL, "workspace too small");
         auto st = static_cast<cudaStream_t>(stream);
-        DeviceCtx& C = ctx();
+        DeviceCtx& C = ctx(st, g->offsets);
         int* s = succ ? succ : center;  // the chase runs in place on center
         cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, 0, g->n, s, 1, g->n, g->nnz, C.pool, st), "successor kernel");
         cuda_check(launch_chase(g->n, n_sigma, s, center, st, workspace), "chase kernel");
@@ -705,7 +733,7 @@ gqc_status gqc_dev_successors(const gqc_csr* g, const double* v, int32_t n_sigma
         if (n_sigma < 1) fail(GQC_EINVAL, "sigma grid is empty");
         if (row_begin < 0 || row_end > g->n || row_begin > row_end) fail(GQC_ERANGE, "row range out of range");
         if (!v || (!succ_rows && row_end > row_begin)) fail(GQC_EINVAL, "null buffer");
-        DeviceCtx& C = ctx();
+        DeviceCtx& C = ctx(static_cast<cudaStream_t>(stream), g->offsets);
         cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, row_begin, row_end, succ_rows,
                                      n_sigma, 1, g->nnz, C.pool, static_cast<cudaStream_t>(stream)),
                    "successor kernel");
@@ -724,6 +752,7 @@ gqc_status gqc_dev_resolve(int32_t n, int32_t n_sigma, const int32_t* succ_nm, i
         if (!succ_nm || !center || !cluster_index || !num_clusters || !workspace) fail(GQC_EINVAL, "null buffer");
         if (workspace_bytes < labels_workspace_bytes(n, n_sigma)) fail(GQC_EINVAL, "workspace too small");
         auto st = static_cast<cudaStream_t>(stream);
+        bind_device(st, succ_nm);
         cuda_check(launch_transpose_i32(succ_nm, n, n_sigma, center, st), "transpose");
         cuda_check(launch_chase(n, n_sigma, center, center, st, workspace), "chase kernel");
         cuda_check(launch_labels(n, n_sigma, center, cluster_index, num_clusters, workspace, workspace_bytes, st, true),
@@ -734,6 +763,7 @@ gqc_status gqc_dev_resolve(int32_t n, int32_t n_sigma, const int32_t* succ_nm, i
 gqc_status gqc_dev_transpose(const double* v_nm, int32_t n, int32_t n_sigma, double* v_sm, void* stream) {
     return guarded([&] {
         if (n < 0 || n_sigma < 1 || !v_nm || !v_sm) fail(GQC_EINVAL, "bad transpose arguments");
+        bind_device(static_cast<cudaStream_t>(stream), v_nm);
         cuda_check(launch_transpose(v_nm, n, n_sigma, v_sm, stream), "transpose");
     });
 }

@@ -36,6 +36,7 @@ KERNEL_FASTFWD = 0
 KERNEL_REPLAY = 1
 _OPT_EXP_MODE = 1
 _OPT_KERNEL = 2
+_OPT_DEVICE = 3
 
 
 class GqcError(Exception):
@@ -167,6 +168,19 @@ def set_exp_mode(mode: int):
 
 def set_kernel(kernel: int):
     _check(_lib.gqc_set_option(_OPT_KERNEL, int(kernel)))
+
+
+def set_device(device: int):
+    """CUDA device of the host-buffer entry points (potentials, cluster_sweep,
+    ...). The dev_* functions follow the device of the stream they are given.
+    libgqc has its own CUDA runtime: torch.cuda.set_device does not reach it."""
+    _check(_lib.gqc_set_option(_OPT_DEVICE, int(device)))
+
+
+def get_device() -> int:
+    v = np.zeros(1, dtype=np.int64)
+    _check(_lib.gqc_get_option(_OPT_DEVICE, _ptr(v)))
+    return int(v[0])
 
 
 def get_options():

@@ -58,6 +58,11 @@ def test_validation_before_device():
     with pytest.raises(ValueError, match="unknown exp mode"):
         N.set_exp_mode(7)
     assert N.get_options() == {"exp_mode": 0, "kernel": 0}
+    with pytest.raises(ValueError, match="device ordinal out of range"):
+        N.set_device(N.device_count() + 3)
+    with pytest.raises(ValueError, match="device ordinal out of range"):
+        N.set_device(-1)
+    assert N.get_device() == 0
 
 
 def test_no_cpu_fallback_without_device():

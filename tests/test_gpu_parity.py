@@ -505,3 +505,27 @@ def test_hub_companion_launch_rows_bitwise(kernel, unit, mode):
     field = N.potentials(g.csr(N), sig)
     for q, s in enumerate(sig[:4]):
         assert_bits(field[q], oracle_field(g, s, mode))
+
+
+def test_device_binding_follows_stream_and_option():
+    # libgqc links its own CUDA runtime: the dev_* entry points bind to the
+    # device of the caller's stream (or buffers), host entry points to
+    # GQC_OPT_DEVICE; both must agree with torch's view of the device
+    import torch
+    g = H.random_graph(501, 5.0, seed=4, unit=True)
+    dg = N.DeviceCsr(g.csr(N), "cuda:0")
+    sig = O.log_sigma_grid(10.0, 8)
+    st = torch.cuda.Stream(device="cuda:0")
+    out = torch.empty((g.n, len(sig)), dtype=torch.float64, device="cuda:0")
+    N.dev_potentials(dg, sig, 0, g.n, out, st)
+    st.synchronize()
+    N.set_device(0)
+    assert N.get_device() == 0
+    host = N.potentials(g.csr(N), sig)
+    assert_bits(out.cpu().numpy().T.copy(), host)
+    out2 = torch.empty_like(out)
+    N.dev_potentials(dg, sig, 0, g.n, out2, None)  # legacy default stream: device of the buffers
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int64), out2.view(torch.int64))
+    with pytest.raises(ValueError):
+        N.set_device(torch.cuda.device_count())
