@@ -13,9 +13,10 @@ step is N^2 * 32 pairs; value = N^2 * 32 / step time, whole job.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
   torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1, NCCL)
 
---impl reference times the reference's CPU path (the oracle restatement of
-compute_potentials_parallel with all host threads; the reference itself does
-not compile here) on a bounded row sample of the same workload.
+--impl reference times the reference's CPU path on a bounded row sample of the
+same workload with all host threads: the reference's own potential code
+(oracle/_ref, built here from /root/reference/proj/src with a restated Eigen
+subset), or the oracle restatement when that was not built.
 """
 from __future__ import annotations
 
@@ -162,17 +163,41 @@ def measured_peaks():
 
 
 # ----------------------------------------------------------------- CPU legs
+_REF_GRAPH = {}
+
+
 def cpu_sample(off, nbr, sigmas, budget_s, threads):
-    """Time the oracle's compute_potentials_parallel restatement (potential.cpp:
-    18-37 per row, contiguous row blocks over `threads` threads) on a
-    deterministic row sample: every k-th row, all sigmas. Returns
-    (pairs/s, rows, elapsed, V_rows[rows][S])."""
+    """Time the reference's CPU potential path on a deterministic row sample
+    (every k-th row, all sigmas), `threads` host threads over contiguous
+    blocks of the sample. Prefers the reference's OWN code (oracle/_ref:
+    /root/reference/proj/src compiled with the restated Eigen subset,
+    graphqc::node_potential = potential.cpp:46-51 -> :18-37 per row); falls
+    back to the oracle restatement of the same loop when that library was not
+    built. Returns (pairs/s, rows, elapsed, V_rows[rows][S], kind, what)."""
     from oracle import pyoracle as O
-    O.build()
+    from oracle import pyref as R
     n = len(off) - 1
+    if R.available():
+        key = (id(off), n)
+        if key not in _REF_GRAPH:
+            _REF_GRAPH.clear()
+            _REF_GRAPH[key] = R.Graph.from_csr(off, nbr, None, W_DEFAULT)
+        g = _REF_GRAPH[key]
+        kind, what = "reference", ("the reference's own graphqc::node_potential (potential.cpp:18-51, compiled from "
+                                   "/root/reference with the restated Eigen subset, SSE2 pexp)")
+
+        def rows_fn(s, rows, workers):
+            return g.node_potentials(s, rows, threads=workers)
+    else:
+        O.build()
+        kind, what = "port", "oracle restatement of potential_at (potential.cpp:18-37, Eigen pexp restated)"
+
+        def rows_fn(s, rows, workers):
+            return O.potentials_rows(off, nbr, None, W_DEFAULT, s, rows, workers=workers)
     # calibrate with one row on one thread
+    rows_fn(sigmas[0], np.array([0], np.int32), 1)
     t0 = time.perf_counter()
-    O.potentials_rows(off, nbr, None, W_DEFAULT, sigmas[0], np.array([0], np.int32), workers=1)
+    rows_fn(sigmas[0], np.array([n // 2], np.int32), 1)
     per_row = max(time.perf_counter() - t0, 1e-6)
     rows_total = max(threads, int(budget_s * threads / per_row))
     per_sigma = max(threads, rows_total // len(sigmas))
@@ -182,10 +207,10 @@ def cpu_sample(off, nbr, sigmas, budget_s, threads):
     out = np.empty((len(rows), len(sigmas)))
     t0 = time.perf_counter()
     for q, s in enumerate(sigmas):
-        out[:, q] = O.potentials_rows(off, nbr, None, W_DEFAULT, s, rows, workers=threads)
+        out[:, q] = rows_fn(s, rows, threads)
     el = time.perf_counter() - t0
     pairs = float(len(rows)) * n * len(sigmas)
-    return pairs / el, rows, el, out
+    return pairs / el, rows, el, out, kind, what
 
 
 def run_reference(args):
@@ -202,15 +227,14 @@ def run_reference(args):
     rows_used = 0
     warm = args.warmup
     for it in range(warm + args.steps):
-        pps, rows, el, _ = cpu_sample(off, nbr, sig, budget, threads)
+        pps, rows, el, _, kind, what = cpu_sample(off, nbr, sig, budget, threads)
         if it >= warm:
             vals.append(pps / 1e9)
             secs.append(el)
             rows_used = len(rows)
     value = statistics.mean(vals)
     sample = (f"{rows_used} evenly strided rows x {len(sig)} sigmas per step "
-              f"({rows_used * n * len(sig):.3e} logical pairs), oracle restatement of "
-              "compute_potentials_parallel (Eigen pexp restated, ascending-j fp64)")
+              f"({rows_used * n * len(sig):.3e} logical pairs), {what}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(secs),
@@ -218,7 +242,7 @@ def run_reference(args):
         "config": {"workload": desc, "n_nodes": n, "nnz": int(len(nbr)), "n_sigma": len(sig),
                    "sigma_grid": f"log_sigma_grid(10, {len(sig)})",
                    "step": "one bounded row sample of the sweep (all sigmas), see cpu_baseline.sample"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -355,12 +379,12 @@ def run_native(args):
     V_host_rows = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         threads = os.cpu_count() or 1
-        pps, srows, el, vref = cpu_sample(off, nbr, sig, args.cpu_seconds, threads)
+        pps, srows, el, vref, kind, what = cpu_sample(off, nbr, sig, args.cpu_seconds, threads)
         V_host_rows = shard.view(-1, S)[torch.from_numpy(srows.astype(np.int64)).to(dev)].cpu().numpy()
         same = bool(np.array_equal(V_host_rows.view(np.int64), vref.view(np.int64)))
-        cpu = {"value": pps / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+        cpu = {"value": pps / 1e9, "unit": UNIT, "cores": threads, "kind": kind,
                "sample": f"{len(srows)} strided rows x {S} sigmas ({len(srows) * n * S:.3e} pairs) in {el:.1f}s, "
-                         f"oracle restatement of compute_potentials_parallel; GPU rows bit-identical: {same}"}
+                         f"{what}; GPU rows bit-identical: {same}"}
 
     if rank == 0:
         line = {

@@ -1,0 +1,261 @@
+// ============================================================================
+// ORACLE / TEST INFRASTRUCTURE ONLY — a C-ABI shim over the reference's OWN
+// library, compiled from /root/reference/proj/src/*.cpp by oracle/Makefile
+// (target `ref`, output oracle/_ref/libgraphqc_ref.so, never committed).
+// Eigen is replaced by oracle/eigen_shim (restated pexp_double; see there).
+//
+// This file contains no reference code: it only calls the reference's public
+// API (include/graphqc/{graph,potential,ggd,metrics,sweep}.hpp) so that
+// tests/ can pin the restatement (oracle.cpp) and the GPU path against the
+// reference's own implementation, and bench.py's reference arm can time the
+// reference's own potential loop (potential.cpp:18-37) on the host cores.
+// Error statuses mirror oracle.cpp: 1 invalid_argument, 2 out_of_range,
+// 3 logic_error, 4 IoError, 9 other.
+// ============================================================================
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "graphqc/ggd.hpp"
+#include "graphqc/graph.hpp"
+#include "graphqc/metrics.hpp"
+#include "graphqc/potential.hpp"
+#include "graphqc/sweep.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const graphqc::IoError& e) {
+        g_err = e.what();
+        return 4;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::out_of_range& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 9;
+    }
+}
+
+void copy_out(const std::string& s, char* buf, std::int64_t cap, std::int64_t* len) {
+    *len = static_cast<std::int64_t>(s.size());
+    if (buf && cap > 0) {
+        const std::int64_t n = std::min<std::int64_t>(cap - 1, *len);
+        std::memcpy(buf, s.data(), static_cast<std::size_t>(n));
+        buf[n] = '\0';
+    }
+}
+
+const graphqc::Graph& G(void* h) { return *static_cast<graphqc::Graph*>(h); }
+
+void fill(const graphqc::ClusterAssignment& c, std::int32_t* center, std::int32_t* cluster_index,
+          std::int32_t* num_clusters) {
+    if (center) std::copy(c.center.begin(), c.center.end(), center);
+    if (cluster_index) std::copy(c.cluster_index.begin(), c.cluster_index.end(), cluster_index);
+    if (num_clusters) *num_clusters = c.num_clusters;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// graphqc::Graph(n, edges, W): the CSR's u < v entries as the edge list.
+void* ref_graph_from_csr(std::int32_t n, const std::int64_t* off, const std::int32_t* nbr, const double* w,
+                         double W) {
+    graphqc::Graph* out = nullptr;
+    const int st = guarded([&] {
+        std::vector<graphqc::Edge> edges;
+        for (std::int32_t u = 0; u < n; ++u)
+            for (std::int64_t k = off[u]; k < off[u + 1]; ++k)
+                if (u < nbr[k]) edges.push_back({u, nbr[k], w ? w[k] : 1.0});
+        out = new graphqc::Graph(n, edges, W);
+    });
+    return st == 0 ? out : nullptr;
+}
+
+void* ref_graph_load(const char* path, double W) {
+    graphqc::Graph* out = nullptr;
+    const int st = guarded([&] { out = new graphqc::Graph(graphqc::load_edge_list(path, W)); });
+    return st == 0 ? out : nullptr;
+}
+
+void ref_graph_free(void* h) { delete static_cast<graphqc::Graph*>(h); }
+
+int ref_graph_shape(void* h, std::int32_t* n, std::int64_t* nnz) {
+    return guarded([&] {
+        *n = G(h).num_nodes();
+        *nnz = 2 * G(h).num_edges();
+    });
+}
+
+int ref_graph_csr(void* h, std::int64_t* off, std::int32_t* nbr, double* w) {
+    return guarded([&] {
+        const auto& g = G(h);
+        off[0] = 0;
+        for (std::int32_t i = 0; i < g.num_nodes(); ++i) {
+            auto ids = g.neighbor_ids(i);
+            auto ws = g.neighbor_weights(i);
+            std::copy(ids.begin(), ids.end(), nbr + off[i]);
+            if (w) std::copy(ws.begin(), ws.end(), w + off[i]);
+            off[i + 1] = off[i] + static_cast<std::int64_t>(ids.size());
+        }
+    });
+}
+
+// compute_potentials (workers == 0) or compute_potentials_parallel.
+int ref_potentials(void* h, double sigma, int workers, double* out) {
+    return guarded([&] {
+        const graphqc::PotentialField pf = workers == 0 ? graphqc::compute_potentials(G(h), sigma)
+                                                        : graphqc::compute_potentials_parallel(G(h), sigma, workers);
+        for (Eigen::Index i = 0; i < pf.values.size(); ++i) out[i] = pf.values[i];
+    });
+}
+
+// node_potential for a list of rows, `threads` host threads over contiguous
+// blocks of the list (the bench's bounded row sample).
+int ref_node_potentials(void* h, double sigma, const std::int32_t* rows, std::int64_t nrows, int threads,
+                        double* out) {
+    return guarded([&] {
+        if (threads < 1) throw std::invalid_argument("threads must be at least 1");
+        std::vector<std::string> errs(threads);
+        auto block = [&](int t) {
+            const std::int64_t b = nrows * t / threads, e = nrows * (t + 1) / threads;
+            try {
+                for (std::int64_t k = b; k < e; ++k) out[k] = graphqc::node_potential(G(h), rows[k], sigma);
+            } catch (const std::exception& ex) {
+                errs[t] = ex.what();
+            }
+        };
+        std::vector<std::jthread> pool;
+        for (int t = 1; t < threads; ++t) pool.emplace_back(block, t);
+        block(0);
+        pool.clear();
+        for (const auto& m : errs)
+            if (!m.empty()) throw std::invalid_argument(m);
+    });
+}
+
+// build_successors + resolve_centers on a given field.
+int ref_ggd(void* h, double sigma, const double* v, std::int32_t* succ, std::int32_t* center,
+            std::int32_t* cluster_index, std::int32_t* num_clusters) {
+    return guarded([&] {
+        const auto& g = G(h);
+        graphqc::PotentialField pf{sigma, g.default_distance(), Eigen::VectorXd(g.num_nodes())};
+        for (std::int32_t i = 0; i < g.num_nodes(); ++i) pf.values[i] = v[i];
+        const graphqc::SuccessorMap s = graphqc::build_successors(g, pf);
+        if (succ) std::copy(s.succ.begin(), s.succ.end(), succ);
+        fill(graphqc::resolve_centers(s), center, cluster_index, num_clusters);
+    });
+}
+
+int ref_cluster(void* h, double sigma, int workers, std::int32_t* center, std::int32_t* cluster_index,
+                std::int32_t* num_clusters) {
+    return guarded([&] { fill(graphqc::cluster(G(h), sigma, workers), center, cluster_index, num_clusters); });
+}
+
+// resolve_centers on an arbitrary successor map (error-order parity).
+int ref_resolve(const std::int32_t* succ, std::int32_t n, std::int32_t* center, std::int32_t* cluster_index,
+                std::int32_t* num_clusters) {
+    return guarded([&] {
+        graphqc::SuccessorMap s;
+        s.succ.assign(succ, succ + n);
+        fill(graphqc::resolve_centers(s), center, cluster_index, num_clusters);
+    });
+}
+
+// evaluate() -> metric_csv_row for an assignment (optional dense labels).
+int ref_metric_row(void* h, const std::int32_t* cluster_index, std::int32_t num_clusters, const std::int32_t* labels,
+                   std::int32_t num_classes, double gamma, double sigma, char* buf, std::int64_t cap,
+                   std::int64_t* len) {
+    return guarded([&] {
+        const auto& g = G(h);
+        graphqc::ClusterAssignment c;
+        c.cluster_index.assign(cluster_index, cluster_index + g.num_nodes());
+        c.num_clusters = num_clusters;
+        std::optional<graphqc::LabelSet> ls;
+        if (labels) {
+            std::vector<std::string> names(num_classes);
+            for (std::int32_t k = 0; k < num_classes; ++k) names[k] = std::to_string(k);
+            ls.emplace(std::vector<std::int32_t>(labels, labels + g.num_nodes()), num_classes, names);
+        }
+        copy_out(graphqc::metric_csv_row(graphqc::evaluate(g, c, ls ? &*ls : nullptr, gamma, sigma)), buf, cap, len);
+    });
+}
+
+// `graphqc cluster` report: header + row (graphqc_main.cpp:86-105 calls
+// load_edge_list, load_labels, cluster, evaluate, metric_csv_*).
+int ref_run_cluster_report(const char* graph_path, const char* labels_path, double sigma, double W, int workers,
+                           double gamma, char* buf, std::int64_t cap, std::int64_t* len) {
+    return guarded([&] {
+        const graphqc::Graph g = graphqc::load_edge_list(graph_path, W);
+        std::optional<graphqc::LabelSet> ls;
+        if (labels_path && *labels_path) ls = graphqc::load_labels(labels_path, g);
+        const auto c = graphqc::cluster(g, sigma, workers);
+        const auto r = graphqc::evaluate(g, c, ls ? &*ls : nullptr, gamma, sigma);
+        copy_out(graphqc::metric_csv_header() + "\n" + graphqc::metric_csv_row(r) + "\n", buf, cap, len);
+    });
+}
+
+// run_sweep over an explicit grid -> write_sweep_csv + detect_mutation.
+int ref_run_sweep(const char* graph_path, const char* labels_path, double W, int workers, double gamma,
+                  const double* sigmas, std::int32_t n_sigma, char* buf, std::int64_t cap, std::int64_t* len,
+                  double* mut_lo, double* mut_hi, std::int32_t* mut_drop, std::int32_t* has_mut) {
+    return guarded([&] {
+        const graphqc::Graph g = graphqc::load_edge_list(graph_path, W);
+        std::optional<graphqc::LabelSet> ls;
+        if (labels_path && *labels_path) ls = graphqc::load_labels(labels_path, g);
+        const auto recs = graphqc::run_sweep(g, std::span<const double>(sigmas, n_sigma), ls ? &*ls : nullptr,
+                                             workers, gamma);
+        std::ostringstream os;
+        graphqc::write_sweep_csv(os, recs);
+        copy_out(os.str(), buf, cap, len);
+        *has_mut = 0;
+        if (recs.size() >= 2) {
+            if (auto m = graphqc::detect_mutation(recs)) {
+                *has_mut = 1;
+                *mut_lo = m->sigma_low;
+                *mut_hi = m->sigma_high;
+                *mut_drop = m->drop;
+            }
+        }
+    });
+}
+
+// gauss = (k * x).exp() through the shim's ArrayXd expression (packets of
+// two + scalar tail), for checking the restated exp against oracle.cpp's.
+int ref_array_exp(const double* x, std::int64_t n, double k, double* out) {
+    return guarded([&] {
+        Eigen::ArrayXd a(n), g;
+        for (std::int64_t i = 0; i < n; ++i) a[i] = x[i];
+        g = (k * a).exp();
+        for (std::int64_t i = 0; i < n; ++i) out[i] = g[i];
+    });
+}
+
+int ref_log_sigma_grid(double W, int steps, double lo_f, double hi_f, double* out) {
+    return guarded([&] {
+        const auto g = graphqc::log_sigma_grid(W, steps, lo_f, hi_f);
+        std::copy(g.begin(), g.end(), out);
+    });
+}
+
+}  // extern "C"
