@@ -87,7 +87,7 @@ def main(tag):
         cpu = d.get("cpu_baseline") or {}
         return (f"| {label} | {d['value']:.4g} GPairs/s, {d['ms_per_step']:.3f} ms/step | "
                 f"{e2e.get('value', float('nan')):.4g} GPairs/s ({e2e.get('ms_per_step', float('nan')):.2f} ms) | "
-                f"{cpu.get('value', float('nan')):.3g} GPairs/s ({cpu.get('cores')} cores) | "
+                f"{cpu.get('value', float('nan')):.3g} GPairs/s ({cpu.get('cores')} cores, {cpu.get('kind')}) | "
                 f"{json.dumps({k: round(v, 3) for k, v in (d.get('breakdown_ms') or {}).items()})} |")
 
     qc = None
@@ -121,7 +121,7 @@ numbers, the profile explains them.
 
 ## Bench lines (1 B200; value = device time with inputs resident, e2e = C-ABI with pinned host buffers)
 
-| workload (32 sigmas, log_sigma_grid(10, 32)) | value | e2e | CPU baseline (oracle port, same run) | breakdown (ms) |
+| workload (32 sigmas, log_sigma_grid(10, 32)) | value | e2e | CPU baseline (same run; kind: reference = the reference's own code, port = oracle) | breakdown (ms) |
 |---|---|---|---|---|
 {line(b, "LFR-style N=1M, nnz 20.0M (headline)")}
 {line(sbm, "planted-partition SBM N=100k, nnz 1.6M")}
