@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--workload", choices=["lfr1m", "sbm100k", "rmat22"], default="lfr1m")
     ap.add_argument("--n-sigma", type=int, default=32)
     ap.add_argument("--kernel", choices=["fastfwd", "replay"], default="fastfwd")
+    ap.add_argument("--hop-cap", type=int, default=1,
+                    help="distance model: 1 = the reference's (default); 2..7 = opt-in k-hop extension")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
@@ -166,7 +168,7 @@ def measured_peaks():
 _REF_GRAPH = {}
 
 
-def cpu_sample(off, nbr, sigmas, budget_s, threads):
+def cpu_sample(off, nbr, sigmas, budget_s, threads, hop_cap=1):
     """Time the reference's CPU potential path on a deterministic row sample
     (every k-th row, all sigmas), `threads` host threads over contiguous
     blocks of the sample. Prefers the reference's OWN code (oracle/_ref:
@@ -177,7 +179,13 @@ def cpu_sample(off, nbr, sigmas, budget_s, threads):
     from oracle import pyoracle as O
     from oracle import pyref as R
     n = len(off) - 1
-    if R.available():
+    if hop_cap > 1:  # k-hop extension: not a reference feature, only the oracle has it
+        O.build()
+        kind, what = "port", f"oracle k-hop restatement (fill_khop, hop cap {hop_cap}) of potential_at"
+
+        def rows_fn(s, rows, workers):
+            return O.potentials_khop(off, nbr, None, W_DEFAULT, s, hop_cap, workers=workers, rows=rows)
+    elif R.available():
         key = (id(off), n)
         if key not in _REF_GRAPH:
             _REF_GRAPH.clear()
@@ -227,7 +235,7 @@ def run_reference(args):
     rows_used = 0
     warm = args.warmup
     for it in range(warm + args.steps):
-        pps, rows, el, _, kind, what = cpu_sample(off, nbr, sig, budget, threads)
+        pps, rows, el, _, kind, what = cpu_sample(off, nbr, sig, budget, threads, args.hop_cap)
         if it >= warm:
             vals.append(pps / 1e9)
             secs.append(el)
@@ -263,6 +271,7 @@ def run_native(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     N.set_kernel(N.KERNEL_FASTFWD if args.kernel == "fastfwd" else N.KERNEL_REPLAY)
+    N.set_hop_cap(args.hop_cap)
     N.set_device(local)  # libgqc's own CUDA runtime: host-API calls on this rank's GPU
 
     off, nbr, desc = make_graph(args.workload)
@@ -367,6 +376,11 @@ def run_native(args):
     # roofline of the dominant kernel (potential sweep, this rank's rows)
     row_nnz = int(off[end] - off[begin])
     alg_bytes = 8 * (rows + 1) + 4 * row_nnz + 8 * rows * S
+    if args.hop_cap > 1:
+        # k-hop pipeline (timed as a whole): both BFS passes read every
+        # neighbour's row (4 B x sum over the rows' neighbours of their degree)
+        deg = np.diff(off).astype(np.int64)
+        alg_bytes += 2 * 4 * int((deg[nbr[off[begin]:off[end]]]).sum())
     peak, peak_kind = measured_peaks()
     achieved = alg_bytes / (pot / 1e3) / 1e9 if pot > 0 else None
 
@@ -379,7 +393,7 @@ def run_native(args):
     V_host_rows = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         threads = os.cpu_count() or 1
-        pps, srows, el, vref, kind, what = cpu_sample(off, nbr, sig, args.cpu_seconds, threads)
+        pps, srows, el, vref, kind, what = cpu_sample(off, nbr, sig, args.cpu_seconds, threads, args.hop_cap)
         V_host_rows = shard.view(-1, S)[torch.from_numpy(srows.astype(np.int64)).to(dev)].cpu().numpy()
         same = bool(np.array_equal(V_host_rows.view(np.int64), vref.view(np.int64)))
         cpu = {"value": pps / 1e9, "unit": UNIT, "cores": threads, "kind": kind,
@@ -393,6 +407,8 @@ def run_native(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": desc, "n_nodes": n, "nnz": int(nnz), "n_sigma": S,
                        "sigma_grid": f"log_sigma_grid(10, {S})", "kernel": args.kernel,
+                       "distance": ("reference (graph.cpp:258-267, hop cap 1)" if args.hop_cap == 1 else
+                                    f"k-hop extension, hop cap {args.hop_cap} (not a reference feature)"),
                        "parallelism": f"potentials row-shard x{world}; all-to-all(V) by sigma chunk; "
                                       f"GGD sigma-shard x{world}; all-gather(labels)",
                        "l2": "512 MiB write between timed steps (excluded from the per-step events)",
@@ -401,9 +417,11 @@ def run_native(args):
             "breakdown_ms": dict(breakdown, wall_s_timed_region=wall),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,
-                         "traffic": recorded_traffic("potential_warp_kernel<FASTFWD,unit>") if world == 1 else None,
+                         "traffic": (recorded_traffic("potential_warp_kernel<FASTFWD,unit>")
+                                     if world == 1 and args.hop_cap == 1 else None),
                          "traffic_source": "profiles/traffic.json (ncu --set full, LFR 1M, 32 sigmas)",
-                         "kernel": "potential_warp_kernel<FASTFWD,unit>",
+                         "kernel": ("potential_warp_kernel<FASTFWD,unit>" if args.hop_cap == 1 else
+                                    "k-hop pipeline (khop_expand x2 + segmented sort + khop_walk_kernel)"),
                          "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
                          "note": "algorithmic bytes = 8(rows+1) + 4*nnz + 8*rows*S; the exact fast-forward is "
                                  "issue-bound (fp64/int chain arithmetic), see DESIGN.md"},

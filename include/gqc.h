@@ -75,7 +75,15 @@ typedef enum gqc_kernel { GQC_KERNEL_FASTFWD = 0, GQC_KERNEL_REPLAY = 1 } gqc_ke
  * they are given (or, for the legacy default stream, of their buffers):
  * libgqc links its own CUDA runtime, so the caller's current device does not
  * carry over. */
-typedef enum gqc_option { GQC_OPT_EXP_MODE = 1, GQC_OPT_KERNEL = 2, GQC_OPT_DEVICE = 3 } gqc_option;
+/* GQC_OPT_HOP_CAP (K, default 1): distance model of every potential entry
+ * point. 1 = the reference's pairwise_distance (graph.cpp:258-267: 0 / edge
+ * weight / W). K in 2..7 = opt-in k-hop extension, NOT in the reference
+ * (SURVEY §8(f)): on unit-weight graphs d(i,j) = BFS hop count for hops
+ * 1..K and W beyond; the sums keep the reference's order and exp rule.
+ * Weighted graphs with K > 1 -> GQC_EINVAL ("k-hop distances need unit
+ * weights"). The fast-forward kernel runs either way (GQC_OPT_KERNEL only
+ * selects the K = 1 kernel). */
+typedef enum gqc_option { GQC_OPT_EXP_MODE = 1, GQC_OPT_KERNEL = 2, GQC_OPT_DEVICE = 3, GQC_OPT_HOP_CAP = 4 } gqc_option;
 
 const char* gqc_last_error(void);
 const char* gqc_version(void);

@@ -347,12 +347,43 @@ struct CsrView {
     const std::int32_t* nbr;
     const double* wt;  // nullptr => unit weights
     double W;
+    int hop_cap = 1;   // 1 = the reference's distance (graph.cpp:258-267); > 1 = k-hop extension below
 };
 
-struct Workspace {  // potential.cpp:12-16
+struct Workspace {  // potential.cpp:12-16 (+ BFS scratch of the k-hop extension)
     std::vector<double> dist2, gauss;
+    std::vector<std::int32_t> hop, frontier, next;
     explicit Workspace(std::int32_t n) : dist2(n), gauss(n) {}
 };
+
+// k-hop distance extension (NOT in the reference, the
+// north star's "multi-source BFS hop distances"): on a unit-weight graph,
+// d(i,j) = 0 for j == i, h for a shortest path of h <= K hops, W otherwise.
+// K = 1 is exactly the reference's pairwise_distance (graph.cpp:258-267,
+// SPEC.md:69-77). The potential loop itself is unchanged (same Eigen
+// packet/tail exp rule, same ascending sums). A plain level-synchronous BFS
+// per row, written as the definition.
+void fill_khop(const CsrView& g, std::int32_t i, Workspace& ws) {
+    ws.hop.assign(g.n, -1);
+    ws.frontier.assign(1, i);
+    ws.hop[i] = 0;
+    for (int h = 1; h <= g.hop_cap && !ws.frontier.empty(); ++h) {
+        ws.next.clear();
+        for (std::int32_t u : ws.frontier)
+            for (std::int64_t k = g.offsets[u]; k < g.offsets[u + 1]; ++k) {
+                const std::int32_t v = g.nbr[k];
+                if (ws.hop[v] < 0) {
+                    ws.hop[v] = h;
+                    ws.next.push_back(v);
+                }
+            }
+        if (h >= 2) {
+            const double d = static_cast<double>(h);
+            for (std::int32_t v : ws.next) ws.dist2[v] = d * d;
+        }
+        ws.frontier.swap(ws.next);
+    }
+}
 
 // potential.cpp:18-37. ExpMode EIGEN: the linear-vectorised Eigen assignment
 // evaluates whole Packet2d packets from index 0 with pexp and the N mod 2
@@ -365,6 +396,7 @@ double potential_at(const CsrView& g, std::int32_t i, double inv, Workspace& ws,
         const double w = g.wt ? g.wt[k] : 1.0;
         ws.dist2[g.nbr[k]] = w * w;
     }
+    if (g.hop_cap > 1) fill_khop(g, i, ws);
     ws.dist2[i] = 0.0;
 
     const double neg = -inv;
@@ -883,6 +915,21 @@ int orc_potentials_rows(std::int32_t n, const std::int64_t* offsets, const std::
                         double W, double sigma, int workers, int mode, const std::int32_t* rows,
                         std::int64_t nrows, double* out) {
     return guarded([&] { potentials_rows(CsrView{n, offsets, nbr, wt, W}, sigma, workers, mode, rows, nrows, out); });
+}
+
+// k-hop extension entry points (hop_cap >= 1; > 1 needs unit weights).
+int orc_potentials_khop(std::int32_t n, const std::int64_t* offsets, const std::int32_t* nbr, const double* wt,
+                        double W, double sigma, int hop_cap, int workers, int mode, const std::int32_t* rows,
+                        std::int64_t nrows, double* out) {
+    return guarded([&] {
+        if (hop_cap < 1 || hop_cap > 7) throw std::invalid_argument("hop cap must be in 1..7");
+        if (hop_cap > 1 && wt)
+            for (std::int64_t k = 0; k < offsets[n]; ++k)
+                if (wt[k] != 1.0) throw std::invalid_argument("k-hop distances need unit weights");
+        CsrView g{n, offsets, nbr, wt, W, hop_cap};
+        if (rows) potentials_rows(g, sigma, workers, mode, rows, nrows, out);
+        else compute_potentials_parallel(g, sigma, workers, mode, out);
+    });
 }
 
 int orc_build_successors(std::int32_t n, const std::int64_t* offsets, const std::int32_t* nbr, const double* v,

@@ -60,6 +60,7 @@ def _declare(L):
     L.orc_csr_from_edges.argtypes = [i32, i64, P, P, P, f64, P, P, P, P]
     L.orc_potentials.argtypes = [i32, P, P, P, f64, f64, C.c_int, C.c_int, P]
     L.orc_potentials_rows.argtypes = [i32, P, P, P, f64, f64, C.c_int, C.c_int, P, i64, P]
+    L.orc_potentials_khop.argtypes = [i32, P, P, P, f64, f64, C.c_int, C.c_int, C.c_int, P, i64, P]
     L.orc_build_successors.argtypes = [i32, P, P, P, P]
     L.orc_resolve_centers.argtypes = [i32, P, P, P, P]
     L.orc_log_sigma_grid.argtypes = [f64, C.c_int, f64, f64, P]
@@ -120,6 +121,17 @@ def potentials_rows(offsets, nbr, wt, W, sigma, rows, workers=1, mode=EXP_EIGEN)
     out = np.empty(len(rows), dtype=np.float64)
     _check(lib().orc_potentials_rows(n, _p(offsets), _p(nbr), _p(wt), W, sigma, workers, mode, _p(rows),
                                      len(rows), _p(out)))
+    return out
+
+
+def potentials_khop(offsets, nbr, wt, W, sigma, hop_cap, workers=1, mode=EXP_EIGEN, rows=None):
+    """k-hop distance extension (oracle.cpp fill_khop): d = hops for 2..hop_cap,
+    W beyond; hop_cap = 1 is the reference's distance. All rows or a row list."""
+    n = len(offsets) - 1
+    r = None if rows is None else np.ascontiguousarray(rows, dtype=np.int32)
+    out = np.empty(n if r is None else len(r), dtype=np.float64)
+    _check(lib().orc_potentials_khop(n, _p(offsets), _p(nbr), _p(wt), W, sigma, hop_cap, workers, mode, _p(r),
+                                     0 if r is None else len(r), _p(out)))
     return out
 
 

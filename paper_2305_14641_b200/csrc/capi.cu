@@ -32,6 +32,7 @@ struct Options {
     int exp_mode = GQC_EXP_EIGEN;
     int kernel = GQC_KERNEL_FASTFWD;
     int device = 0;  // device of the host-buffer entry points (GQC_OPT_DEVICE)
+    int hop_cap = 1;  // distance model (GQC_OPT_HOP_CAP): 1 = the reference's
 } g_opt;
 
 struct Fail {
@@ -245,6 +246,9 @@ void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S,
     const int mode = g_opt.exp_mode;
     const bool weighted = g.w != nullptr;
     const bool tail = (mode == GQC_EXP_EIGEN) && (n % 2 == 1);
+    const int K = g_opt.hop_cap;
+    if (K > 1 && weighted) fail(GQC_EINVAL, "k-hop distances need unit weights");
+    if (K > 1 && n >= (1 << 29)) fail(GQC_EINVAL, "k-hop distances need fewer than 2^29 nodes");
 
     // weighted graphs: the glibc-evaluated entries the device cannot produce
     std::vector<double> last_w;        // weights of row n-1 (Eigen tail)
@@ -307,6 +311,13 @@ void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S,
         for (int s = 0; s < Sc; ++s) {
             P.c[s] = make_sigma_consts(sigmas[s0 + s], g.W, mode);
             neg_inv[s] = P.c[s].neg_inv;
+        }
+        if (K > 1) {  // k-hop extension (khop.cu)
+            P.weight_mode = kUnit;
+            KhopTable t{};
+            for (int s = 0; s < Sc; ++s) fill_khop_table(t, s, sigmas[s0 + s], K, mode);
+            cuda_check(launch_potentials_khop(P, K, t, C.pool, st), "k-hop potential launch");
+            continue;
         }
         if (!weighted) {
             P.weight_mode = kUnit;
@@ -415,6 +426,9 @@ gqc_status gqc_set_option(gqc_option key, int64_t value) {
         } else if (key == GQC_OPT_KERNEL) {
             if (value != GQC_KERNEL_FASTFWD && value != GQC_KERNEL_REPLAY) fail(GQC_EINVAL, "unknown kernel");
             g_opt.kernel = static_cast<int>(value);
+        } else if (key == GQC_OPT_HOP_CAP) {
+            if (value < 1 || value > kMaxHopCap) fail(GQC_EINVAL, "hop cap must be in 1..7");
+            g_opt.hop_cap = static_cast<int>(value);
         } else if (key == GQC_OPT_DEVICE) {
             int count = 0;
             if (cudaGetDeviceCount(&count) != cudaSuccess) {
@@ -435,6 +449,7 @@ gqc_status gqc_get_option(gqc_option key, int64_t* value) {
         if (key == GQC_OPT_EXP_MODE) *value = g_opt.exp_mode;
         else if (key == GQC_OPT_KERNEL) *value = g_opt.kernel;
         else if (key == GQC_OPT_DEVICE) *value = g_opt.device;
+        else if (key == GQC_OPT_HOP_CAP) *value = g_opt.hop_cap;
         else fail(GQC_EINVAL, "unknown option");
     });
 }
@@ -543,6 +558,7 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
         const int n = g->n;
         const long long nnz = g->nnz;
         const bool weighted = g->w && !all_unit(g->w, nnz);
+        if (g_opt.hop_cap > 1 && weighted) fail(GQC_EINVAL, "k-hop distances need unit weights");
 
         // Pipeline: the CSR goes up in row slabs on the copy stream while the
         // compute stream runs the potentials of the slabs already resident
@@ -567,7 +583,8 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
                                "copy weights");
             }
         }
-        const int slabs = nnz >= (1 << 20) ? 4 : 1;
+        // (k-hop rows read their neighbours' rows too: one slab, the whole CSR)
+        const int slabs = (nnz >= (1 << 20) && g_opt.hop_cap == 1) ? 4 : 1;
         std::vector<int> bound(slabs + 1, n);
         bound[0] = 0;
         for (int k = 1; k < slabs; ++k)  // equal-nnz row slabs

@@ -82,6 +82,19 @@ int resolve_checked(std::int32_t n, const std::int32_t* succ_dev, std::int32_t* 
                     std::int32_t* cluster_index_dev, std::int32_t* num_clusters_host, int* err_kind, void* pool,
                     void* stream);
 
+// k-hop extension (khop.cu): per-sigma constants of a hop-h term,
+// d2 = h*h: e = exp(-inv*d2) by the exp provider, p = d2*e; "t" = the glibc
+// values of the Eigen tail column. Index 0 unused; h = 1 equals (e1, p1).
+constexpr int kMaxHopCap = 7;
+struct KhopTable {
+    double e[kMaxHopCap + 1][kMaxSigmaPerLaunch];
+    double p[kMaxHopCap + 1][kMaxSigmaPerLaunch];
+    double et[kMaxHopCap + 1][kMaxSigmaPerLaunch];
+    double pt[kMaxHopCap + 1][kMaxSigmaPerLaunch];
+};
+void fill_khop_table(KhopTable& t, int s, double sigma, int hop_cap, int exp_mode);
+int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTable& t, void* pool, void* stream);
+
 // Launch accounting (kernels issued by the last C-ABI call).
 void count_launch(int k = 1);
 

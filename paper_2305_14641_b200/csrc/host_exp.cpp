@@ -81,4 +81,20 @@ SigmaConsts make_sigma_consts(double sigma, double W, int exp_mode) {
     return c;
 }
 
+// k-hop extension: the hop-h term of the reference loop with dist2 = h*h
+// (potential.cpp:26, :32-33 with d = h): e = exp((-inv) * d2), p = d2 * e.
+void fill_khop_table(KhopTable& t, int s, double sigma, int hop_cap, int exp_mode) {
+    const double neg = -inv_two_sigma_sq(sigma);
+    for (int h = 0; h <= kMaxHopCap; ++h) {
+        const double d = static_cast<double>(h);
+        const double d2 = d * d;
+        const double a = neg * d2;
+        const bool used = h >= 1 && h <= hop_cap;
+        t.e[h][s] = used ? (exp_mode == 0 ? host_pexp(a) : host_glibc_exp(a)) : 0.0;
+        t.p[h][s] = d2 * t.e[h][s];
+        t.et[h][s] = used ? host_glibc_exp(a) : 0.0;
+        t.pt[h][s] = d2 * t.et[h][s];
+    }
+}
+
 }  // namespace gqc

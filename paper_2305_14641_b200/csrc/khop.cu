@@ -1,0 +1,418 @@
+// k-hop distance extension of the potential sweep (opt-in, GQC_OPT_HOP_CAP).
+//
+// NOT in the reference: its distance is hop-capped at 1 (graph.cpp:258-267,
+// SPEC.md:69-77). This is SURVEY §8(f) row 4, the north star's "multi-source
+// BFS hop distances over CSR": on a unit-weight graph d(i,j) = 0 for j == i,
+// the BFS hop count h for 1 <= h <= K, and W beyond K or when unreachable.
+// K = 1 is exactly the reference's distance (and runs the main kernels). The
+// per-row sums keep the reference's contract unchanged: ascending j, fp64,
+// Eigen packet exp + glibc tail column (oracle.cpp fill_khop is the checker).
+//
+// Pipeline per launch (rows [row_begin, row_end)):
+//   1. khop_expand_kernel<false>: BFS from every source row to depth K with
+//      the visited set as a bitset in shared memory (one per block; global
+//      memory when N bits do not fit): warp-per-frontier-vertex expansion,
+//      each neighbour row read as coalesced 32-wide chunks, atomicOr into the
+//      bitset, and warp-ballot compaction of the newly reached columns into
+//      the next frontier. Counts the nodes at hops 2..K per row.
+//   2. exclusive scan of the counts -> event offsets (int64);
+//   3. khop_expand_kernel<true>: the same BFS, writing each row's hop >= 2
+//      nodes as events (col << 3 | hop) into its segment;
+//   4. cub segmented sort of the events by column (row segments);
+//   5. khop_walk_kernel: warp = one row x 32 sigma lanes, the same exact
+//      run fast-forward as the main kernel (ff_chain.cuh) over the merge of
+//      the CSR row (hop 1) and the sorted events (hop >= 2), longest rows
+//      first. Rows are processed in batches that bound the event memory.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+
+#include "gqc_internal.h"
+#include "ff_chain.cuh"
+
+namespace gqc {
+namespace {
+
+using namespace gqc::ffc;
+
+constexpr int kExpandThreads = 512;
+constexpr int kWalkBlock = 256;
+constexpr int kWalkBlocksPerSM = 4;
+constexpr unsigned kFull = 0xffffffffu;
+// Shared-memory bitset limit per block (bits of N): N <= 1.6M keeps it on chip.
+constexpr std::size_t kSmemBitsetBytes = 200 * 1024;
+// Events held in device memory at once (keys + sorted keys): 2 x 4 B each.
+constexpr long long kEventBudget = 1ll << 30;
+
+struct KhopExpand {
+    int n;
+    const long long* off;
+    const int* nbr;
+    int row_begin, rows;  // this pass covers rows [row_begin, row_begin + rows)
+    int K;
+    int* counter;              // row queue
+    long long* count;          // count pass: hop >= 2 nodes of each row
+    const long long* ev_off;   // fill pass: event offset of each row (absolute)
+    long long ev_base;         // fill pass: ev_off value of the pass's first row
+    unsigned* ev;              // fill pass: events (col << 3 | hop), relative to ev_base
+    unsigned* scratch;         // count pass: [gridDim.x][n] per-block level lists
+    unsigned* gbits;           // [gridDim.x][words] global bitsets, or nullptr (shared)
+    int words;
+};
+
+template <bool kFill>
+__global__ void __launch_bounds__(kExpandThreads) khop_expand_kernel(const KhopExpand E) {
+    extern __shared__ unsigned sbits[];
+    __shared__ int s_row, s_pos;
+    unsigned* bits = E.gbits ? E.gbits + static_cast<std::size_t>(blockIdx.x) * E.words : sbits;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    for (int w = tid; w < E.words; w += blockDim.x) bits[w] = 0u;
+    __syncthreads();
+    for (;;) {
+        if (tid == 0) {
+            s_row = atomicAdd(E.counter, 1);
+            s_pos = 0;
+        }
+        __syncthreads();
+        const int r = s_row;
+        if (r >= E.rows) break;
+        const int i = E.row_begin + r;
+        const long long kb = E.off[i], ke = E.off[i + 1];
+        unsigned* dst = kFill ? E.ev + (E.ev_off[r] - E.ev_base)
+                              : E.scratch + static_cast<std::size_t>(blockIdx.x) * E.n;
+        // hop 0 and 1: the row itself and its CSR neighbours
+        if (tid == 0) atomicOr(&bits[i >> 5], 1u << (i & 31));
+        for (long long k = kb + tid; k < ke; k += blockDim.x) {
+            const int c = E.nbr[k];
+            atomicOr(&bits[c >> 5], 1u << (c & 31));
+        }
+        __syncthreads();
+        int lvl_b = 0, lvl_e = 0;
+        for (int h = 2; h <= E.K; ++h) {
+            const long long nf = (h == 2) ? (ke - kb) : (lvl_e - lvl_b);
+            // warp per frontier vertex: its row in coalesced 32-wide chunks
+            for (long long f = warp; f < nf; f += nwarps) {
+                const int u = (h == 2) ? E.nbr[kb + f] : static_cast<int>(dst[lvl_b + f] >> 3);
+                const long long ub = E.off[u], ue = E.off[u + 1];
+                for (long long k = ub; k < ue; k += 32) {
+                    const bool valid = k + lane < ue;
+                    const int c = valid ? E.nbr[k + lane] : 0;
+                    bool fresh = false;
+                    if (valid) {
+                        const unsigned bit = 1u << (c & 31);
+                        fresh = !(atomicOr(&bits[c >> 5], bit) & bit);
+                    }
+                    const unsigned m = __ballot_sync(kFull, fresh);
+                    if (m) {  // ballot compaction of the newly reached columns
+                        int base = 0;
+                        if (lane == 0) base = atomicAdd(&s_pos, __popc(m));
+                        base = __shfl_sync(kFull, base, 0);
+                        if (fresh) dst[base + __popc(m & ((1u << lane) - 1u))] = (static_cast<unsigned>(c) << 3) | h;
+                    }
+                }
+            }
+            __syncthreads();
+            lvl_b = lvl_e;
+            lvl_e = s_pos;
+            __syncthreads();  // every thread has read s_pos before the next level appends
+        }
+        if (!kFill && tid == 0) E.count[r] = lvl_e;
+        // clear the words this row touched
+        if (tid == 0) bits[i >> 5] = 0u;
+        for (long long k = kb + tid; k < ke; k += blockDim.x) bits[E.nbr[k] >> 5] = 0u;
+        for (int q = tid; q < lvl_e; q += blockDim.x) bits[(dst[q] >> 3) >> 5] = 0u;
+        __syncthreads();
+    }
+}
+
+__global__ void khop_segments_kernel(const long long* __restrict__ ev_off, int rows, int* __restrict__ seg) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k <= rows) seg[k] = static_cast<int>(ev_off[k] - ev_off[0]);
+}
+
+__global__ void khop_keys_kernel(const long long* __restrict__ off, const long long* __restrict__ count, int row_begin,
+                                 int rows, int* __restrict__ key, int* __restrict__ id) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= rows) return;
+    const int i = row_begin + k;
+    const long long w = (off[i + 1] - off[i]) + count[k];
+    key[k] = static_cast<int>(min(w, static_cast<long long>(INT_MAX)));
+    id[k] = k;
+}
+
+__device__ __forceinline__ long long out_slot(const PotentialLaunch& P, const int i, const int s) {
+    const int k = P.out_col0 + s;
+    const int q = k / P.out_chunk;
+    return q * P.out_chunk_stride + static_cast<long long>(i - P.row_begin) * P.out_ld + (k - q * P.out_chunk);
+}
+
+// Walk of rows whose batch-relative index comes from `order` (heaviest
+// first): lane s = sigma s, the merge of hop-1 (CSR) and hop >= 2 (events)
+// columns is warp-uniform.
+__global__ void __launch_bounds__(kWalkBlock, kWalkBlocksPerSM)
+    khop_walk_kernel(const __grid_constant__ PotentialLaunch P, const __grid_constant__ KhopTable T,
+                     const unsigned* __restrict__ ev, const int* __restrict__ seg, int batch_row0,
+                     const int* __restrict__ order, int rows, int* __restrict__ counter) {
+    // per-sigma constants staged in shared memory (lane-indexed reads of the
+    // kernel parameters would serialise on the constant cache)
+    __shared__ double sc[6][kMaxSigmaPerLaunch];
+    __shared__ double st[4][kMaxHopCap + 1][kMaxSigmaPerLaunch];
+    const int S = P.n_sigma;
+    for (int idx = threadIdx.x; idx < kMaxSigmaPerLaunch; idx += blockDim.x) {
+        const int q = min(idx, S - 1);
+        sc[0][idx] = P.c[q].pW;
+        sc[1][idx] = P.c[q].eW;
+        sc[2][idx] = P.c[q].pWt;
+        sc[3][idx] = P.c[q].eWt;
+        sc[4][idx] = P.c[q].inv;
+    }
+    for (int idx = threadIdx.x; idx < (kMaxHopCap + 1) * kMaxSigmaPerLaunch; idx += blockDim.x) {
+        const int h = idx / kMaxSigmaPerLaunch, q = idx % kMaxSigmaPerLaunch;
+        st[0][h][q] = T.e[h][q];
+        st[1][h][q] = T.p[h][q];
+        st[2][h][q] = T.et[h][q];
+        st[3][h][q] = T.pt[h][q];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int s = min(lane, S - 1);
+    const double pW = sc[0][s], eW = sc[1][s];
+    const int n = P.n;
+    const bool tail = P.tail != 0;
+    for (;;) {
+        int g0 = 0;
+        if (lane == 0) g0 = atomicAdd(counter, 1);
+        const int g = __shfl_sync(kFull, g0, 0);
+        if (g >= rows) break;
+        const int rb = order[g];                   // batch-relative row
+        const int i = P.row_begin + batch_row0 + rb;
+        Chain num = make_chain(0.0, pW), den = make_chain(0.0, eW);
+        int pos = 0;
+        bool self_pending = true;
+        auto w_run = [&](const int L) {
+            if (L <= 0) return;
+            if (pos == 0) {  // first run: from s = 0 (general loop)
+                ff_run(num, pW, L);
+                ff_run(den, eW, L);
+                num.top = 0.0;
+                den.top = 0.0;
+            } else {
+                ff_walk2(num, pW, den, eW, L);
+            }
+        };
+        auto add_self = [&]() {
+            w_run(i - pos);
+            den.s = __dadd_rn(den.s, 1.0);  // d2 = 0: num += 0, den += exp(0) = 1
+            pos = i + 1;
+            self_pending = false;
+        };
+        auto event = [&](const int col, const int h) {
+            if (self_pending && i < col) add_self();
+            w_run(col - pos);
+            const bool at_tail = tail && col == n - 1;
+            const double e = st[at_tail ? 2 : 0][h][s];
+            const double p = st[at_tail ? 3 : 1][h][s];
+            num.s = __dadd_rn(num.s, p);
+            den.s = __dadd_rn(den.s, e);
+            pos = col + 1;
+        };
+        // merge hop 1 (CSR row, ascending) with hop >= 2 (sorted events)
+        long long ka = P.offsets[i];
+        const long long ka_end = P.offsets[i + 1];
+        long long kb = seg[rb];
+        const long long kb_end = seg[rb + 1];
+        long long base_a = ka, base_b = kb;
+        int buf_a = (ka + lane < ka_end) ? __ldg(P.nbr + ka + lane) : INT_MAX;
+        unsigned buf_b = (kb + lane < kb_end) ? __ldg(ev + kb + lane) : 0xffffffffu;
+        while (ka < ka_end || kb < kb_end) {  // warp-uniform
+            const int ca = __shfl_sync(kFull, buf_a, static_cast<int>(ka - base_a));
+            const unsigned eb = __shfl_sync(kFull, buf_b, static_cast<int>(kb - base_b));
+            const int cb = kb < kb_end ? static_cast<int>(eb >> 3) : INT_MAX;
+            if (ka < ka_end && ca < cb) {
+                event(ca, 1);
+                if (++ka - base_a == 32) {
+                    base_a = ka;
+                    buf_a = (ka + lane < ka_end) ? __ldg(P.nbr + ka + lane) : INT_MAX;
+                }
+            } else {
+                event(cb, static_cast<int>(eb & 7u));
+                if (++kb - base_b == 32) {
+                    base_b = kb;
+                    buf_b = (kb + lane < kb_end) ? __ldg(ev + kb + lane) : 0xffffffffu;
+                }
+            }
+        }
+        if (self_pending) add_self();
+        const int L = n - pos;  // final run; the Eigen tail column n-1 uses glibc constants
+        if (L > 0) {
+            if (tail) {
+                w_run(L - 1);
+                num.s = __dadd_rn(num.s, sc[2][s]);
+                den.s = __dadd_rn(den.s, sc[3][s]);
+            } else {
+                w_run(L);
+            }
+        }
+        if (lane < S) P.out[out_slot(P, i, s)] = __dmul_rn(sc[4][s], __ddiv_rn(num.s, den.s));
+    }
+}
+
+int num_sms() {
+    static int v = 0;
+    if (!v) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return v;
+}
+
+}  // namespace
+
+int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTable& T, void* pool_, void* stream) {
+    const int rows = p.row_end - p.row_begin;
+    if (rows <= 0) return cudaSuccess;
+    auto st = static_cast<cudaStream_t>(stream);
+    auto pool = static_cast<cudaMemPool_t>(pool_);
+    cudaError_t e;
+    const int n = p.n;
+    const int words = (n + 31) / 32;
+    const std::size_t bitset_bytes = static_cast<std::size_t>(words) * 4;
+    const bool smem = bitset_bytes <= kSmemBitsetBytes;
+    const int dyn = smem ? static_cast<int>(bitset_bytes) : 0;
+    int per_sm = 1;
+    cudaFuncSetAttribute(khop_expand_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    cudaFuncSetAttribute(khop_expand_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, khop_expand_kernel<false>, kExpandThreads, dyn);
+    const int grid = std::max(1, std::min(num_sms() * std::max(per_sm, 1), rows));
+
+    // scratch: counter, counts/offsets, per-block level lists, global bitsets
+    auto bytes_of = [](std::size_t b) { return (b + 255) & ~static_cast<std::size_t>(255); };
+    const std::size_t b_cnt = bytes_of(16), b_count = bytes_of((rows + 1) * sizeof(long long));
+    const std::size_t b_off = b_count;
+    const std::size_t b_scr = bytes_of(static_cast<std::size_t>(grid) * n * sizeof(unsigned));
+    const std::size_t b_bits = smem ? 0 : bytes_of(static_cast<std::size_t>(grid) * bitset_bytes);
+    std::size_t scan_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, static_cast<long long*>(nullptr),
+                                  static_cast<long long*>(nullptr), rows + 1);
+    void* mem = nullptr;
+    if ((e = cudaMallocFromPoolAsync(&mem, b_cnt + b_count + b_off + b_scr + b_bits + bytes_of(scan_bytes), pool,
+                                     st)) != cudaSuccess)
+        return e;
+    char* m = static_cast<char*>(mem);
+    int* counter = reinterpret_cast<int*>(m);
+    long long* count = reinterpret_cast<long long*>(m + b_cnt);
+    long long* ev_off = reinterpret_cast<long long*>(m + b_cnt + b_count);
+    unsigned* scratch = reinterpret_cast<unsigned*>(m + b_cnt + b_count + b_off);
+    unsigned* gbits = smem ? nullptr : reinterpret_cast<unsigned*>(m + b_cnt + b_count + b_off + b_scr);
+    void* scan_tmp = m + b_cnt + b_count + b_off + b_scr + b_bits;
+
+    KhopExpand E{};
+    E.n = n;
+    E.off = reinterpret_cast<const long long*>(p.offsets);
+    E.nbr = p.nbr;
+    E.K = hop_cap;
+    E.count = count;
+    E.scratch = scratch;
+    E.gbits = gbits;
+    E.words = words;
+    E.counter = counter;
+    E.row_begin = p.row_begin;
+    E.rows = rows;
+    cudaMemsetAsync(counter, 0, 16, st);
+    cudaMemsetAsync(count + rows, 0, sizeof(long long), st);
+    khop_expand_kernel<false><<<grid, kExpandThreads, dyn, st>>>(E);
+    count_launch();
+    if ((e = cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, count, ev_off, rows + 1, st)) != cudaSuccess)
+        return e;
+    count_launch();
+
+    // batches of rows whose events fit the budget
+    std::vector<long long> h_off(rows + 1);
+    if ((e = cudaMemcpyAsync(h_off.data(), ev_off, (rows + 1) * sizeof(long long), cudaMemcpyDeviceToHost, st)) !=
+        cudaSuccess)
+        return e;
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    std::vector<int> cuts{0};
+    while (cuts.back() < rows) {
+        const int r0 = cuts.back();
+        int r1 = static_cast<int>(std::upper_bound(h_off.begin() + r0 + 1, h_off.end(), h_off[r0] + kEventBudget) -
+                                  h_off.begin()) - 1;
+        cuts.push_back(std::max(r1, r0 + 1));  // a single row always fits (< N events)
+    }
+
+    int walk_grid_cap = num_sms() * kWalkBlocksPerSM;
+    for (std::size_t b = 0; b + 1 < cuts.size(); ++b) {
+        const int r0 = cuts[b], r1 = cuts[b + 1], nr = r1 - r0;
+        const long long items = h_off[r1] - h_off[r0];
+        std::size_t sort_bytes = 0, key_bytes = 0;
+        cub::DeviceSegmentedSort::SortKeys(nullptr, sort_bytes, static_cast<const unsigned*>(nullptr),
+                                           static_cast<unsigned*>(nullptr), static_cast<int>(items), nr,
+                                           static_cast<const int*>(nullptr), static_cast<const int*>(nullptr), st);
+        cub::DeviceRadixSort::SortPairsDescending(nullptr, key_bytes, static_cast<const int*>(nullptr),
+                                                  static_cast<int*>(nullptr), static_cast<const int*>(nullptr),
+                                                  static_cast<int*>(nullptr), nr);
+        const std::size_t b_ev = bytes_of(std::max<long long>(items, 1) * sizeof(unsigned));
+        const std::size_t b_seg = bytes_of((nr + 1) * sizeof(int));
+        const std::size_t b_key = bytes_of(nr * sizeof(int));
+        void* bm = nullptr;
+        if ((e = cudaMallocFromPoolAsync(&bm, 2 * b_ev + b_seg + 4 * b_key + bytes_of(sort_bytes) +
+                                                  bytes_of(key_bytes) + 256,
+                                         pool, st)) != cudaSuccess)
+            return e;
+        char* q = static_cast<char*>(bm);
+        unsigned* ev_raw = reinterpret_cast<unsigned*>(q);
+        unsigned* ev_sorted = reinterpret_cast<unsigned*>(q + b_ev);
+        int* seg = reinterpret_cast<int*>(q + 2 * b_ev);
+        int* key_in = reinterpret_cast<int*>(q + 2 * b_ev + b_seg);
+        int* key_out = key_in + b_key / sizeof(int);
+        int* id_in = key_out + b_key / sizeof(int);
+        int* id_out = id_in + b_key / sizeof(int);
+        int* wcounter = reinterpret_cast<int*>(q + 2 * b_ev + b_seg + 4 * b_key);
+        void* sort_tmp = q + 2 * b_ev + b_seg + 4 * b_key + 256;
+        void* key_tmp = static_cast<char*>(sort_tmp) + bytes_of(sort_bytes);
+
+        // fill pass over the batch's rows
+        KhopExpand F = E;
+        F.row_begin = p.row_begin + r0;
+        F.rows = nr;
+        F.ev_off = ev_off + r0;
+        F.ev_base = h_off[r0];
+        F.ev = ev_raw;
+        cudaMemsetAsync(counter, 0, 16, st);
+        khop_expand_kernel<true><<<std::max(1, std::min(grid, nr)), kExpandThreads, dyn, st>>>(F);
+        count_launch();
+        khop_segments_kernel<<<(nr + 1 + 255) / 256, 256, 0, st>>>(ev_off + r0, nr, seg);
+        count_launch();
+        if (items > 0) {
+            if ((e = cub::DeviceSegmentedSort::SortKeys(sort_tmp, sort_bytes, ev_raw, ev_sorted,
+                                                        static_cast<int>(items), nr, seg, seg + 1, st)) !=
+                cudaSuccess)
+                return e;
+            count_launch();
+        }
+        // longest rows first
+        khop_keys_kernel<<<(nr + 255) / 256, 256, 0, st>>>(E.off, count + r0, p.row_begin + r0, nr, key_in, id_in);
+        count_launch();
+        if ((e = cub::DeviceRadixSort::SortPairsDescending(key_tmp, key_bytes, key_in, key_out, id_in, id_out, nr, 0,
+                                                           32, st)) != cudaSuccess)
+            return e;
+        count_launch(2);
+        cudaMemsetAsync(wcounter, 0, sizeof(int), st);
+        const int wgrid = static_cast<int>(
+            std::min<long long>((nr + kWalkBlock / 32 - 1) / (kWalkBlock / 32), walk_grid_cap));
+        khop_walk_kernel<<<wgrid, kWalkBlock, 0, st>>>(p, T, ev_sorted, seg, r0, id_out, nr, wcounter);
+        count_launch();
+        cudaFreeAsync(bm, st);
+    }
+    cudaFreeAsync(mem, st);
+    return cudaGetLastError();
+}
+
+}  // namespace gqc

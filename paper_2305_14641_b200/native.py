@@ -37,6 +37,7 @@ KERNEL_REPLAY = 1
 _OPT_EXP_MODE = 1
 _OPT_KERNEL = 2
 _OPT_DEVICE = 3
+_OPT_HOP_CAP = 4
 
 
 class GqcError(Exception):
@@ -177,6 +178,19 @@ def set_device(device: int):
     _check(_lib.gqc_set_option(_OPT_DEVICE, int(device)))
 
 
+def set_hop_cap(k: int):
+    """Distance model of the potential entry points: 1 = the reference's
+    (graph.cpp:258-267); 2..7 = the opt-in k-hop extension (BFS hop counts up
+    to k, W beyond; unit-weight graphs only). Not a reference feature."""
+    _check(_lib.gqc_set_option(_OPT_HOP_CAP, int(k)))
+
+
+def get_hop_cap() -> int:
+    v = np.zeros(1, dtype=np.int64)
+    _check(_lib.gqc_get_option(_OPT_HOP_CAP, _ptr(v)))
+    return int(v[0])
+
+
 def get_device() -> int:
     v = np.zeros(1, dtype=np.int64)
     _check(_lib.gqc_get_option(_OPT_DEVICE, _ptr(v)))
@@ -188,7 +202,9 @@ def get_options():
     _check(_lib.gqc_get_option(_OPT_EXP_MODE, _ptr(v)))
     mode = int(v[0])
     _check(_lib.gqc_get_option(_OPT_KERNEL, _ptr(v)))
-    return {"exp_mode": mode, "kernel": int(v[0])}
+    kernel = int(v[0])
+    _check(_lib.gqc_get_option(_OPT_HOP_CAP, _ptr(v)))
+    return {"exp_mode": mode, "kernel": kernel, "hop_cap": int(v[0])}
 
 
 def device_count() -> int:

@@ -57,7 +57,13 @@ def test_validation_before_device():
         N.build_successors(g, np.zeros(3))
     with pytest.raises(ValueError, match="unknown exp mode"):
         N.set_exp_mode(7)
-    assert N.get_options() == {"exp_mode": 0, "kernel": 0}
+    assert N.get_options() == {"exp_mode": 0, "kernel": 0, "hop_cap": 1}
+    for bad in (0, 8, -1):
+        with pytest.raises(ValueError, match="hop cap must be in 1..7"):
+            N.set_hop_cap(bad)
+    N.set_hop_cap(3)
+    assert N.get_hop_cap() == 3
+    N.set_hop_cap(1)
     with pytest.raises(ValueError, match="device ordinal out of range"):
         N.set_device(N.device_count() + 3)
     with pytest.raises(ValueError, match="device ordinal out of range"):

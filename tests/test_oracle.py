@@ -163,3 +163,37 @@ def test_oracle_vs_definition():
             e = np.exp(-d2 / (2 * sigma * sigma))
             ref = (d2 * e).sum() / e.sum() / (2 * sigma * sigma)
             assert abs(v[i] - ref) <= 1e-12 * max(abs(ref), 1e-300)
+
+
+def test_khop_oracle_matches_definition_and_reference_distance():
+    """k-hop extension (oracle.cpp fill_khop): hop_cap 1 is the reference's
+    distance bit for bit; hop_cap K matches a direct restatement of the
+    definition (networkx BFS hop counts, W beyond K, the Eigen packet / glibc
+    tail exp rule, ascending fp64 sums) on small graphs."""
+    import networkx as nx
+    for n, deg, seed in [(41, 3, 1), (40, 2, 2), (57, 5, 3)]:
+        g = H.random_graph(n, deg, seed, unit=True)
+        for sigma in (0.7, 2.0, 6.0):
+            base = O.potentials(g.offsets, g.nbr, g.wt, g.W, sigma)
+            k1 = O.potentials_khop(g.offsets, g.nbr, g.wt, g.W, sigma, 1)
+            assert np.array_equal(base.view(np.int64), k1.view(np.int64))
+        G = nx.Graph()
+        G.add_nodes_from(range(n))
+        for i in range(n):
+            for k in range(g.offsets[i], g.offsets[i + 1]):
+                G.add_edge(i, int(g.nbr[k]))
+        for K in (2, 3, 5):
+            got = O.potentials_khop(g.offsets, g.nbr, g.wt, g.W, 2.5, K, workers=2)
+            inv = 1.0 / (2.0 * 2.5 * 2.5)
+            for i in range(n):
+                hops = nx.single_source_shortest_path_length(G, i, cutoff=K)
+                d2 = [float(hops[j]) ** 2 if j in hops else g.W * g.W for j in range(n)]
+                ex = [O.eigen_pexp(-inv * x) if j < n - n % 2 else O.glibc_exp(-inv * x) for j, x in enumerate(d2)]
+                num = den = 0.0
+                for x, e in zip(d2, ex):
+                    num += x * e
+                    den += e
+                assert got[i] == inv * (num / den)
+    with pytest.raises(ValueError, match="k-hop distances need unit weights"):
+        w = H.random_graph(30, 3, 9, unit=False)
+        O.potentials_khop(w.offsets, w.nbr, w.wt, w.W, 1.0, 2)
