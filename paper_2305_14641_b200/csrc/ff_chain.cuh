@@ -361,6 +361,97 @@ GQC_HD inline double walk_events(double s, const double c, const double c1, cons
 }
 
 // ---------------------------------------------------------------------------
+// Batched walk over events of NC classes (the k-hop extension: class h = a
+// hop-h term). Same rule as walk_events with one increment per class: inside
+// a binade where c and every class constant cc[k] are jumpable and none is a
+// half-ulp tie there, the sum after event q is exactly
+//     s + A(q) * inc + sum_k B_k(q) * inc_k,
+// A = W columns in [pos, col(q)), B_k = class-k events in [e, q]. Every
+// partial value of the fma chain is a u-grid point no larger than the final
+// one, so all are exact while the final stays below top, and monotone
+// rounding keeps the "< top" test exact when it does not. Ev provides
+// col(q), cls(q) in [0, NC) and cnt(q, k) = class-k events among [0, q] of
+// the current chunk (cnt(-1, k) = 0).
+// ---------------------------------------------------------------------------
+template <int NC, class Ev>
+GQC_HD inline double walk_events_multi(double s, const double c, const int tie_c, const double* cc,
+                                       const int* tie_cc, const Ev& ev, int e, const int end, int pos) {
+    while (e < end) {
+        GQC_WALK_COUNT();
+        const int f = gqc_max(exp_field(s), 1);
+        const double base = pow2_field(f);
+        const double top = gqc_add(base, base);
+        const double half = gqc_mul(base, 0.5);
+        bool ok = c < half && f != tie_c;
+#pragma unroll
+        for (int k = 0; k < NC; ++k) ok = ok && cc[k] < half && f != tie_cc[k];
+        if (ok) {
+            const double inc = gqc_sub(gqc_add(base, c), base);
+            double inck[NC];
+            int b0[NC];
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+                inck[k] = gqc_sub(gqc_add(base, cc[k]), base);
+                b0[k] = ev.cnt(e - 1, k);
+            }
+            auto value = [&](const int q) {
+                double t = gqc_fma(static_cast<double>(ev.col(q) - pos - (q - e)), inc, s);
+#pragma unroll
+                for (int k = 0; k < NC; ++k) t = gqc_fma(static_cast<double>(ev.cnt(q, k) - b0[k]), inck[k], t);
+                return t;
+            };
+            int lo = e - 1, hi = end - 1;  // last event whose sum stays below top (e - 1: none)
+            if (value(hi) < top) lo = hi;  // common case: the rest of the range stays in the binade
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (value(mid) < top) lo = mid;
+                else hi = mid - 1;
+            }
+            if (lo >= e) {
+                s = value(lo);
+                pos = ev.col(lo) + 1;
+                e = lo + 1;
+                if (e == end) break;
+            }
+            // event e leaves the binade: inside its W run or at its own term
+            const int ce = ev.col(e);
+            const int L = ce - pos;
+            const double t = gqc_fma(static_cast<double>(L), inc, s);
+            if (t < top) {
+                s = t;
+            } else {
+                Chain ch;
+                ch.s = s;
+                ch.top = top;
+                ch.inc = inc;
+                ch.f_tie = tie_c;
+                ch.flags = kJump;
+                const double m = max_steps(ch, room_of(ch));
+                ch.s = gqc_add(gqc_fma(m, inc, s), c);
+                ch.top = 0.0;
+                ff_run(ch, c, L - static_cast<int>(m) - 1);
+                s = ch.s;
+            }
+            s = gqc_add(s, cc[ev.cls(e)]);
+            pos = ce + 1;
+            ++e;
+        } else {  // one event at a time (tiny sums, tie binades)
+            const int ce = ev.col(e);
+            if (ce > pos) {
+                Chain ch = make_chain(s, c);
+                ch.f_tie = tie_c;
+                ff_run(ch, c, ce - pos);
+                s = ch.s;
+            }
+            s = gqc_add(s, cc[ev.cls(e)]);
+            pos = ce + 1;
+            ++e;
+        }
+    }
+    return s;
+}
+
+// ---------------------------------------------------------------------------
 // Prefix segments of the pure trajectory P(t) = t sequential adds of c from
 // s = 0 (every row's first run, before its first neighbour or itself, is such
 // a run). Segment k covers [t[k], t[k+1]) with P(t) = s0[k] + (t - t[k])*inc[k]

@@ -152,9 +152,26 @@ __device__ __forceinline__ long long out_slot(const PotentialLaunch& P, const in
     return q * P.out_chunk_stride + static_cast<long long>(i - P.row_begin) * P.out_ld + (k - q * P.out_chunk);
 }
 
+// Chunk of up to 32 merged events staged per warp for the batched walk:
+// classes 0 = hop 1 (CSR), 1 = hop 2; cnt(q, k) from the class ballots.
+struct ChunkEvents {
+    const int* cols;
+    const unsigned char* kls;
+    unsigned m0, m1;
+    __device__ int col(int q) const { return cols[q]; }
+    __device__ int cls(int q) const { return kls[q]; }
+    __device__ int cnt(int q, int k) const {
+        const unsigned upto = q < 0 ? 0u : (0xffffffffu >> (31 - q));
+        return __popc((k ? m1 : m0) & upto);
+    }
+};
+
 // Walk of rows whose batch-relative index comes from `order` (heaviest
 // first): lane s = sigma s, the merge of hop-1 (CSR) and hop >= 2 (events)
-// columns is warp-uniform.
+// columns is warp-uniform. kBatch (hop cap 2): the merged events are taken
+// 32 at a time and walked with walk_events_multi (batched in-binade jumps,
+// ff_chain.cuh); otherwise one event at a time.
+template <bool kBatch>
 __global__ void __launch_bounds__(kWalkBlock, kWalkBlocksPerSM)
     khop_walk_kernel(const __grid_constant__ PotentialLaunch P, const __grid_constant__ KhopTable T,
                      const unsigned* __restrict__ ev, const int* __restrict__ seg, int batch_row0,
@@ -179,6 +196,9 @@ __global__ void __launch_bounds__(kWalkBlock, kWalkBlocksPerSM)
         st[2][h][q] = T.et[h][q];
         st[3][h][q] = T.pt[h][q];
     }
+    constexpr int kWarps = kWalkBlock / 32;
+    __shared__ int s_a[kBatch ? kWarps : 1][32], s_b[kBatch ? kWarps : 1][32], s_cols[kBatch ? kWarps : 1][32];
+    __shared__ unsigned char s_kls[kBatch ? kWarps : 1][32];
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int s = min(lane, S - 1);
@@ -227,24 +247,94 @@ __global__ void __launch_bounds__(kWalkBlock, kWalkBlocksPerSM)
         const long long ka_end = P.offsets[i + 1];
         long long kb = seg[rb];
         const long long kb_end = seg[rb + 1];
-        long long base_a = ka, base_b = kb;
-        int buf_a = (ka + lane < ka_end) ? __ldg(P.nbr + ka + lane) : INT_MAX;
-        unsigned buf_b = (kb + lane < kb_end) ? __ldg(ev + kb + lane) : 0xffffffffu;
-        while (ka < ka_end || kb < kb_end) {  // warp-uniform
-            const int ca = __shfl_sync(kFull, buf_a, static_cast<int>(ka - base_a));
-            const unsigned eb = __shfl_sync(kFull, buf_b, static_cast<int>(kb - base_b));
-            const int cb = kb < kb_end ? static_cast<int>(eb >> 3) : INT_MAX;
-            if (ka < ka_end && ca < cb) {
-                event(ca, 1);
-                if (++ka - base_a == 32) {
-                    base_a = ka;
-                    buf_a = (ka + lane < ka_end) ? __ldg(P.nbr + ka + lane) : INT_MAX;
+        if constexpr (kBatch) {
+            const int wslot = threadIdx.x >> 5;
+            int* a_s = s_a[wslot];
+            int* b_s = s_b[wslot];
+            int* cols = s_cols[wslot];
+            unsigned char* kls = s_kls[wslot];
+            const double cn[2] = {st[1][1][s], st[1][2][s]}, cd[2] = {st[0][1][s], st[0][2][s]};
+            const int tn[2] = {tie_binade(cn[0]), tie_binade(cn[1])}, td[2] = {tie_binade(cd[0]), tie_binade(cd[1])};
+            const int tie_pW = tie_binade(pW), tie_eW = tie_binade(eW);
+            while (ka < ka_end || kb < kb_end) {  // warp-uniform
+                // next 32 events of the merge: ranks within the two 32-windows
+                const int a_l = (ka + lane < ka_end) ? __ldg(P.nbr + ka + lane) : INT_MAX;
+                const int b_l = (kb + lane < kb_end) ? static_cast<int>(__ldg(ev + kb + lane) >> 3) : INT_MAX;
+                __syncwarp();
+                a_s[lane] = a_l;
+                b_s[lane] = b_l;
+                __syncwarp();
+                int lo = 0, hi = 32;  // #b < a_l
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (b_s[mid] < a_l) lo = mid + 1;
+                    else hi = mid;
                 }
-            } else {
-                event(cb, static_cast<int>(eb & 7u));
-                if (++kb - base_b == 32) {
-                    base_b = kb;
-                    buf_b = (kb + lane < kb_end) ? __ldg(ev + kb + lane) : 0xffffffffu;
+                const int pa = lane + lo;
+                lo = 0;
+                hi = 32;  // #a < b_l
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (a_s[mid] < b_l) lo = mid + 1;
+                    else hi = mid;
+                }
+                const int pb = lane + lo;
+                const bool va = a_l != INT_MAX && pa < 32, vb = b_l != INT_MAX && pb < 32;
+                if (va) {
+                    cols[pa] = a_l;
+                    kls[pa] = 0;
+                }
+                if (vb) {
+                    cols[pb] = b_l;
+                    kls[pb] = 1;
+                }
+                const unsigned ma = __ballot_sync(kFull, va), mb = __ballot_sync(kFull, vb);
+                ka += __popc(ma);
+                kb += __popc(mb);
+                const int cnt = __popc(ma) + __popc(mb);
+                __syncwarp();
+                const int my = lane < cnt ? cols[lane] : INT_MAX;
+                ChunkEvents ce{cols, kls, __ballot_sync(kFull, lane < cnt && kls[lane] == 0),
+                               __ballot_sync(kFull, lane < cnt && kls[lane] == 1)};
+                const int jend = (tail && cols[cnt - 1] == n - 1) ? cnt - 1 : cnt;
+                const int before_self = __popc(__ballot_sync(kFull, my < i));
+                int j = 0;
+                while (j < jend) {  // warp-uniform
+                    int r = jend;
+                    if (self_pending) r = min(max(before_self, j), jend);
+                    if (r > j) {
+                        num.s = walk_events_multi<2>(num.s, pW, tie_pW, cn, tn, ce, j, r, pos);
+                        den.s = walk_events_multi<2>(den.s, eW, tie_eW, cd, td, ce, j, r, pos);
+                        num.top = 0.0;  // binade caches are stale now
+                        den.top = 0.0;
+                        pos = cols[r - 1] + 1;
+                        j = r;
+                    }
+                    if (self_pending && j < jend) add_self();
+                }
+                if (jend < cnt) event(cols[cnt - 1], kls[cnt - 1] + 1);  // the Eigen tail column
+                __syncwarp();
+            }
+        } else {
+            long long base_a = ka, base_b = kb;
+            int buf_a = (ka + lane < ka_end) ? __ldg(P.nbr + ka + lane) : INT_MAX;
+            unsigned buf_b = (kb + lane < kb_end) ? __ldg(ev + kb + lane) : 0xffffffffu;
+            while (ka < ka_end || kb < kb_end) {  // warp-uniform
+                const int ca = __shfl_sync(kFull, buf_a, static_cast<int>(ka - base_a));
+                const unsigned eb = __shfl_sync(kFull, buf_b, static_cast<int>(kb - base_b));
+                const int cb = kb < kb_end ? static_cast<int>(eb >> 3) : INT_MAX;
+                if (ka < ka_end && ca < cb) {
+                    event(ca, 1);
+                    if (++ka - base_a == 32) {
+                        base_a = ka;
+                        buf_a = (ka + lane < ka_end) ? __ldg(P.nbr + ka + lane) : INT_MAX;
+                    }
+                } else {
+                    event(cb, static_cast<int>(eb & 7u));
+                    if (++kb - base_b == 32) {
+                        base_b = kb;
+                        buf_b = (kb + lane < kb_end) ? __ldg(ev + kb + lane) : 0xffffffffu;
+                    }
                 }
             }
         }
@@ -407,7 +497,10 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
         cudaMemsetAsync(wcounter, 0, sizeof(int), st);
         const int wgrid = static_cast<int>(
             std::min<long long>((nr + kWalkBlock / 32 - 1) / (kWalkBlock / 32), walk_grid_cap));
-        khop_walk_kernel<<<wgrid, kWalkBlock, 0, st>>>(p, T, ev_sorted, seg, r0, id_out, nr, wcounter);
+        if (hop_cap == 2)
+            khop_walk_kernel<true><<<wgrid, kWalkBlock, 0, st>>>(p, T, ev_sorted, seg, r0, id_out, nr, wcounter);
+        else
+            khop_walk_kernel<false><<<wgrid, kWalkBlock, 0, st>>>(p, T, ev_sorted, seg, r0, id_out, nr, wcounter);
         count_launch();
         cudaFreeAsync(bm, st);
     }

@@ -404,3 +404,127 @@ extern "C" long long fft_walk_row_iters(double c, double c1, double cself, const
     *out = walk_row(c, c1, cself, nb, deg, self, ncols);
     return g_walk_iters;
 }
+
+// Multi-class batched walk (walk_events_multi, the k-hop extension): rows of
+// W runs, events of NC = 2 or 3 classes with their own constants, the self
+// term, walked in chunks of 32 events split at the self column like the
+// kernel, against naive sequential adds. Returns mismatches.
+namespace {
+template <int NC>
+struct ChunkEv {
+    const int* cols;
+    const int* kls;
+    int cnt_tab[33][NC];  // cnt_tab[q + 1][k] = class-k events among [0, q]
+    int col(int q) const { return cols[q]; }
+    int cls(int q) const { return kls[q]; }
+    int cnt(int q, int k) const { return cnt_tab[q + 1][k]; }
+};
+
+template <int NC>
+double walk_row_multi(double c, const double* cc, double cself, const int* nb, const int* kl, int deg, int self,
+                      int ncols) {
+    int tie[NC];
+    for (int k = 0; k < NC; ++k) tie[k] = tie_binade(cc[k]);
+    const int tc = tie_binade(c);
+    double s = 0.0;
+    int pos = 0;
+    bool self_pending = true;
+    for (int b = 0; b < deg; b += 32) {
+        const int n = std::min(32, deg - b);
+        ChunkEv<NC> ev{nb + b, kl + b, {}};
+        for (int q = 0; q < n; ++q)
+            for (int k = 0; k < NC; ++k) ev.cnt_tab[q + 1][k] = ev.cnt_tab[q][k] + (kl[b + q] == k);
+        int j = 0;
+        while (j < n) {
+            int r = n;
+            if (self_pending) {
+                r = j;
+                while (r < n && nb[b + r] < self) ++r;
+            }
+            if (r > j) {
+                s = walk_events_multi<NC>(s, c, tc, cc, tie, ev, j, r, pos);
+                pos = nb[b + r - 1] + 1;
+                j = r;
+            }
+            if (self_pending && j < n) {
+                Chain ch = make_chain(s, c);
+                ff_run(ch, c, self - pos);
+                s = ch.s + cself;
+                pos = self + 1;
+                self_pending = false;
+            }
+        }
+    }
+    Chain ch = make_chain(s, c);
+    if (self_pending) {
+        ff_run(ch, c, self - pos);
+        ch.s = ch.s + cself;
+        pos = self + 1;
+        ch.top = 0.0;
+    }
+    ff_run(ch, c, ncols - pos);
+    return ch.s;
+}
+
+double naive_row_multi(double c, const double* cc, double cself, const int* nb, const int* kl, int deg, int self,
+                       int ncols) {
+    double s = 0.0;
+    int k = 0;
+    for (int j = 0; j < ncols; ++j) {
+        if (j == self) s = s + cself;
+        else if (k < deg && nb[k] == j) s = s + cc[kl[k]], ++k;
+        else s = s + c;
+    }
+    return s;
+}
+}  // namespace
+
+extern "C" long long fft_walk_multi(std::uint64_t seed, int nrows, int ncols, int nc, double* bad) {
+    Rng r{seed};
+    long long mism = 0;
+    std::vector<int> nb, kl;
+    for (int row = 0; row < nrows; ++row) {
+        const int deg = r.below(3) == 0 ? r.below(3000) : r.below(300);
+        const int self = r.below(ncols);
+        nb.clear();
+        for (int q = 0; q < deg; ++q) {
+            const int j = r.below(ncols);
+            if (j != self) nb.push_back(j);
+        }
+        std::sort(nb.begin(), nb.end());
+        nb.erase(std::unique(nb.begin(), nb.end()), nb.end());
+        kl.resize(nb.size());
+        for (auto& x : kl) x = r.below(nc);
+        double c, cc[3];
+        if (r.below(2)) {  // QC constants of a random sigma: W term, hop 1..nc terms (num or den)
+            const double sigma = 0.05 + 40.0 * r.uni();
+            const double inv = 1.0 / (2.0 * sigma * sigma);
+            const bool numer = r.below(2);
+            c = std::exp(-inv * 100.0) * (numer ? 100.0 : 1.0);
+            for (int k = 0; k < 3; ++k) {
+                const double d2 = static_cast<double>((k + 1) * (k + 1));
+                cc[k] = std::exp(-inv * d2) * (numer ? d2 : 1.0);
+            }
+        } else {
+            const int ec = 1 + r.below(1060);
+            c = rand_double(r, ec, ec);
+            for (int k = 0; k < 3; ++k) cc[k] = rand_double(r, ec + r.below(45), ec + 45);
+            if (r.below(8) == 0) cc[0] = c;
+            if (r.below(8) == 0) cc[1] = cc[0];
+        }
+        const double cself = r.below(2) ? 1.0 : 0.0;
+        const int d = static_cast<int>(nb.size());
+        const double got = nc == 2 ? walk_row_multi<2>(c, cc, cself, nb.data(), kl.data(), d, self, ncols)
+                                   : walk_row_multi<3>(c, cc, cself, nb.data(), kl.data(), d, self, ncols);
+        const double ref = naive_row_multi(c, cc, cself, nb.data(), kl.data(), d, self, ncols);
+        if (std::memcmp(&got, &ref, sizeof ref) != 0) {
+            if (mism == 0 && bad) {
+                bad[0] = c;
+                bad[1] = cc[0];
+                bad[2] = row;
+            }
+            ++mism;
+        }
+    }
+    return mism;
+}

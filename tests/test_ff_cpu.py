@@ -89,3 +89,14 @@ def test_batched_row_walk_bitwise(ff, seed, ncols):
     bad = np.zeros(3)
     m = ff.fft_walk(seed, 2000, ncols, bad.ctypes.data_as(C.c_void_p), None)
     assert m == 0, f"{m} mismatches, first (c, c1, row) = {bad.tolist()}"
+
+
+@pytest.mark.parametrize("seed,ncols,nc", [(31, 5000, 2), (32, 200000, 2), (33, 60, 2), (34, 20000, 3),
+                                           (35, 1000000, 2), (36, 7, 3)])
+def test_multi_class_batched_walk_bitwise(ff, seed, ncols, nc):
+    # walk_events_multi (k-hop extension: one increment per event class) vs naive adds
+    ff.fft_walk_multi.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_void_p]
+    ff.fft_walk_multi.restype = C.c_longlong
+    bad = np.zeros(3)
+    m = ff.fft_walk_multi(seed, 1500, ncols, nc, bad.ctypes.data_as(C.c_void_p))
+    assert m == 0, f"{m} mismatching rows, first: c={bad[0]!r} c1={bad[1]!r} row={int(bad[2])}"
