@@ -9,15 +9,17 @@
 // Eigen packet exp + glibc tail column (oracle.cpp fill_khop is the checker).
 //
 // Pipeline per launch (rows [row_begin, row_end)):
-//   1. khop_expand_kernel<false>: BFS from every source row to depth K with
-//      the visited set as a bitset in shared memory (one per block; global
-//      memory when N bits do not fit): warp-per-frontier-vertex expansion,
-//      each neighbour row read as coalesced 32-wide chunks, atomicOr into the
-//      bitset, and warp-ballot compaction of the newly reached columns into
-//      the next frontier. Counts the nodes at hops 2..K per row.
+//   1. K >= 3: khop_expand_kernel<false>: BFS from every source row to depth
+//      K with the visited set as a bitset in shared memory (one per block;
+//      global memory when N bits do not fit): warp-per-frontier-vertex
+//      expansion, each neighbour row read as coalesced 32-wide chunks,
+//      atomicOr into the bitset, and warp-ballot compaction of the newly
+//      reached columns into the next frontier. Counts the nodes at hops 2..K
+//      per row. K = 2: no BFS, the sum of the neighbours' degrees bounds the
+//      count (khop_bound_kernel);
 //   2. exclusive scan of the counts -> event offsets (int64);
 //   3. khop_expand_kernel<true>: the same BFS, writing each row's hop >= 2
-//      nodes as events (col << 3 | hop) into its segment;
+//      nodes as events (col << 3 | hop) into its segment, and the count;
 //   4. cub segmented sort of the events by column (row segments);
 //   5. khop_walk_kernel: warp = one row x 32 sigma lanes, the same exact
 //      run fast-forward as the main kernel (ff_chain.cuh) over the merge of
@@ -57,7 +59,7 @@ struct KhopExpand {
     int row_begin, rows;  // this pass covers rows [row_begin, row_begin + rows)
     int K;
     int* counter;              // row queue
-    long long* count;          // count pass: hop >= 2 nodes of each row
+    long long* count;          // hop >= 2 nodes of each row (both passes write it)
     const long long* ev_off;   // fill pass: event offset of each row (absolute)
     long long ev_base;         // fill pass: ev_off value of the pass's first row
     unsigned* ev;              // fill pass: events (col << 3 | hop), relative to ev_base
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(kExpandThreads) khop_expand_kernel(const KhopE
             lvl_e = s_pos;
             __syncthreads();  // every thread has read s_pos before the next level appends
         }
-        if (!kFill && tid == 0) E.count[r] = lvl_e;
+        if (tid == 0) E.count[r] = lvl_e;
         // clear the words this row touched
         if (tid == 0) bits[i >> 5] = 0u;
         for (long long k = kb + tid; k < ke; k += blockDim.x) bits[E.nbr[k] >> 5] = 0u;
@@ -131,9 +133,31 @@ __global__ void __launch_bounds__(kExpandThreads) khop_expand_kernel(const KhopE
     }
 }
 
-__global__ void khop_segments_kernel(const long long* __restrict__ ev_off, int rows, int* __restrict__ seg) {
+// Row segments of a batch relative to its first row: [seg_b, seg_e) = the
+// events the fill pass wrote (offsets may be upper bounds, hop cap 2).
+__global__ void khop_segments_kernel(const long long* __restrict__ ev_off, const long long* __restrict__ count,
+                                     int rows, int* __restrict__ seg_b, int* __restrict__ seg_e) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k <= rows) seg[k] = static_cast<int>(ev_off[k] - ev_off[0]);
+    if (k < rows) {
+        seg_b[k] = static_cast<int>(ev_off[k] - ev_off[0]);
+        seg_e[k] = seg_b[k] + static_cast<int>(count[k]);
+    }
+}
+
+// Hop cap 2: an upper bound of each row's hop-2 count without a BFS pass,
+// the sum of its neighbours' degrees (warp per row).
+__global__ void khop_bound_kernel(const long long* __restrict__ off, const int* __restrict__ nbr, int row_begin,
+                                  int rows, long long* __restrict__ bound) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    const int i = row_begin + w;
+    long long acc = 0;
+    for (long long k = off[i] + lane; k < off[i + 1]; k += 32) {
+        const int u = nbr[k];
+        acc += off[u + 1] - off[u];
+    }
+    for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    if (lane == 0) bound[w] = acc;
 }
 
 __global__ void khop_keys_kernel(const long long* __restrict__ off, const long long* __restrict__ count, int row_begin,
@@ -174,7 +198,8 @@ struct ChunkEvents {
 template <bool kBatch>
 __global__ void __launch_bounds__(kWalkBlock, kWalkBlocksPerSM)
     khop_walk_kernel(const __grid_constant__ PotentialLaunch P, const __grid_constant__ KhopTable T,
-                     const unsigned* __restrict__ ev, const int* __restrict__ seg, int batch_row0,
+                     const unsigned* __restrict__ ev, const int* __restrict__ seg_b,
+                     const int* __restrict__ seg_e, int batch_row0,
                      const int* __restrict__ order, int rows, int* __restrict__ counter) {
     // per-sigma constants staged in shared memory (lane-indexed reads of the
     // kernel parameters would serialise on the constant cache)
@@ -245,8 +270,8 @@ __global__ void __launch_bounds__(kWalkBlock, kWalkBlocksPerSM)
         // merge hop 1 (CSR row, ascending) with hop >= 2 (sorted events)
         long long ka = P.offsets[i];
         const long long ka_end = P.offsets[i + 1];
-        long long kb = seg[rb];
-        const long long kb_end = seg[rb + 1];
+        long long kb = seg_b[rb];
+        const long long kb_end = seg_e[rb];
         if constexpr (kBatch) {
             const int wslot = threadIdx.x >> 5;
             int* a_s = s_a[wslot];
@@ -386,7 +411,7 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
     auto bytes_of = [](std::size_t b) { return (b + 255) & ~static_cast<std::size_t>(255); };
     const std::size_t b_cnt = bytes_of(16), b_count = bytes_of((rows + 1) * sizeof(long long));
     const std::size_t b_off = b_count;
-    const std::size_t b_scr = bytes_of(static_cast<std::size_t>(grid) * n * sizeof(unsigned));
+    const std::size_t b_scr = hop_cap == 2 ? 0 : bytes_of(static_cast<std::size_t>(grid) * n * sizeof(unsigned));
     const std::size_t b_bits = smem ? 0 : bytes_of(static_cast<std::size_t>(grid) * bitset_bytes);
     std::size_t scan_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, static_cast<long long*>(nullptr),
@@ -417,7 +442,12 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
     E.rows = rows;
     cudaMemsetAsync(counter, 0, 16, st);
     cudaMemsetAsync(count + rows, 0, sizeof(long long), st);
-    khop_expand_kernel<false><<<grid, kExpandThreads, dyn, st>>>(E);
+    if (hop_cap == 2) {
+        // no counting BFS: segments sized by the neighbour-degree bound
+        khop_bound_kernel<<<(rows + 7) / 8, 256, 0, st>>>(E.off, E.nbr, p.row_begin, rows, count);
+    } else {
+        khop_expand_kernel<false><<<grid, kExpandThreads, dyn, st>>>(E);
+    }
     count_launch();
     if ((e = cub::DeviceScan::ExclusiveSum(scan_tmp, scan_bytes, count, ev_off, rows + 1, st)) != cudaSuccess)
         return e;
@@ -449,7 +479,7 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
                                                   static_cast<int*>(nullptr), static_cast<const int*>(nullptr),
                                                   static_cast<int*>(nullptr), nr);
         const std::size_t b_ev = bytes_of(std::max<long long>(items, 1) * sizeof(unsigned));
-        const std::size_t b_seg = bytes_of((nr + 1) * sizeof(int));
+        const std::size_t b_seg = 2 * bytes_of((nr + 1) * sizeof(int));
         const std::size_t b_key = bytes_of(nr * sizeof(int));
         void* bm = nullptr;
         if ((e = cudaMallocFromPoolAsync(&bm, 2 * b_ev + b_seg + 4 * b_key + bytes_of(sort_bytes) +
@@ -459,7 +489,8 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
         char* q = static_cast<char*>(bm);
         unsigned* ev_raw = reinterpret_cast<unsigned*>(q);
         unsigned* ev_sorted = reinterpret_cast<unsigned*>(q + b_ev);
-        int* seg = reinterpret_cast<int*>(q + 2 * b_ev);
+        int* seg_b = reinterpret_cast<int*>(q + 2 * b_ev);
+        int* seg_e = seg_b + b_seg / (2 * sizeof(int));
         int* key_in = reinterpret_cast<int*>(q + 2 * b_ev + b_seg);
         int* key_out = key_in + b_key / sizeof(int);
         int* id_in = key_out + b_key / sizeof(int);
@@ -475,14 +506,15 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
         F.ev_off = ev_off + r0;
         F.ev_base = h_off[r0];
         F.ev = ev_raw;
+        F.count = count + r0;
         cudaMemsetAsync(counter, 0, 16, st);
         khop_expand_kernel<true><<<std::max(1, std::min(grid, nr)), kExpandThreads, dyn, st>>>(F);
         count_launch();
-        khop_segments_kernel<<<(nr + 1 + 255) / 256, 256, 0, st>>>(ev_off + r0, nr, seg);
+        khop_segments_kernel<<<(nr + 255) / 256, 256, 0, st>>>(ev_off + r0, count + r0, nr, seg_b, seg_e);
         count_launch();
         if (items > 0) {
             if ((e = cub::DeviceSegmentedSort::SortKeys(sort_tmp, sort_bytes, ev_raw, ev_sorted,
-                                                        static_cast<int>(items), nr, seg, seg + 1, st)) !=
+                                                        static_cast<int>(items), nr, seg_b, seg_e, st)) !=
                 cudaSuccess)
                 return e;
             count_launch();
@@ -498,9 +530,9 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
         const int wgrid = static_cast<int>(
             std::min<long long>((nr + kWalkBlock / 32 - 1) / (kWalkBlock / 32), walk_grid_cap));
         if (hop_cap == 2)
-            khop_walk_kernel<true><<<wgrid, kWalkBlock, 0, st>>>(p, T, ev_sorted, seg, r0, id_out, nr, wcounter);
+            khop_walk_kernel<true><<<wgrid, kWalkBlock, 0, st>>>(p, T, ev_sorted, seg_b, seg_e, r0, id_out, nr, wcounter);
         else
-            khop_walk_kernel<false><<<wgrid, kWalkBlock, 0, st>>>(p, T, ev_sorted, seg, r0, id_out, nr, wcounter);
+            khop_walk_kernel<false><<<wgrid, kWalkBlock, 0, st>>>(p, T, ev_sorted, seg_b, seg_e, r0, id_out, nr, wcounter);
         count_launch();
         cudaFreeAsync(bm, st);
     }
