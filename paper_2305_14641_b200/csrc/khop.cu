@@ -135,6 +135,85 @@ __global__ void __launch_bounds__(kExpandThreads) khop_expand_kernel(const KhopE
 
 // Row segments of a batch relative to its first row: [seg_b, seg_e) = the
 // events the fill pass wrote (offsets may be upper bounds, hop cap 2).
+// Hop cap 2 with the bitset on chip: the events are emitted already sorted.
+// Block per source row (rows from a queue): every neighbour's row is OR-ed
+// into the shared-memory bitset (warp per neighbour, coalesced 32-wide
+// chunks), the row itself and its neighbours are cleared again, and the
+// bitset is scanned in column order: warp w owns a contiguous word range,
+// counts its bits, the warps' counts are scanned, then each warp writes its
+// columns in ascending order (lane-parallel popc + warp scan) and zeroes
+// the words it read. No per-row sort and no second BFS.
+template <int kThreads>
+__global__ void __launch_bounds__(kThreads) khop2_emit_kernel(const KhopExpand E) {
+    extern __shared__ unsigned bits[];
+    __shared__ int s_row;
+    __shared__ int s_tot[kThreads / 32];
+    constexpr int kWarps = kThreads / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = ((E.words + kWarps - 1) / kWarps + 31) & ~31;  // words per warp, multiple of 32
+    for (int w = tid; w < E.words; w += kThreads) bits[w] = 0u;
+    __syncthreads();
+    for (;;) {
+        if (tid == 0) s_row = atomicAdd(E.counter, 1);
+        __syncthreads();
+        const int r = s_row;
+        if (r >= E.rows) break;
+        const int i = E.row_begin + r;
+        const long long kb = E.off[i], ke = E.off[i + 1];
+        for (long long f = warp; f < ke - kb; f += kWarps) {  // warp per neighbour
+            const int u = E.nbr[kb + f];
+            const long long ub = E.off[u], ue = E.off[u + 1];
+            for (long long k = ub + lane; k < ue; k += 32) {
+                const int c = E.nbr[k];
+                atomicOr(&bits[c >> 5], 1u << (c & 31));
+            }
+        }
+        __syncthreads();
+        for (long long k = kb + tid; k < ke; k += kThreads) {  // hop 1 is not a hop-2 event
+            const int c = E.nbr[k];
+            atomicAnd(&bits[c >> 5], ~(1u << (c & 31)));
+        }
+        if (tid == 0) atomicAnd(&bits[i >> 5], ~(1u << (i & 31)));
+        __syncthreads();
+        const int w0 = warp * per, w1 = min(E.words, w0 + per);
+        int cnt = 0;
+        for (int x = w0 + lane; x < w1; x += 32) cnt += __popc(bits[x]);
+        for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(kFull, cnt, d);
+        if (lane == 0) s_tot[warp] = cnt;
+        __syncthreads();
+        int base = 0;
+        for (int q = 0; q < warp; ++q) base += s_tot[q];
+        unsigned* dst = E.ev + (E.ev_off[r] - E.ev_base);
+        for (int x0 = w0; x0 < w1; x0 += 32) {
+            const int x = x0 + lane;
+            unsigned v = x < w1 ? bits[x] : 0u;
+            const int c = __popc(v);
+            int incl = c;
+            for (int d = 1; d < 32; d <<= 1) {
+                const int t = __shfl_up_sync(kFull, incl, d);
+                if (lane >= d) incl += t;
+            }
+            int pos = base + incl - c;
+            if (v) {
+                bits[x] = 0u;
+                const unsigned col0 = static_cast<unsigned>(x) << 5;
+                while (v) {
+                    const int b = __ffs(v) - 1;
+                    dst[pos++] = ((col0 + b) << 3) | 2u;
+                    v &= v - 1;
+                }
+            }
+            base += __shfl_sync(kFull, incl, 31);
+        }
+        if (tid == 0) {
+            int tot = 0;
+            for (int q = 0; q < kWarps; ++q) tot += s_tot[q];
+            E.count[r] = tot;
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void khop_segments_kernel(const long long* __restrict__ ev_off, const long long* __restrict__ count,
                                      int rows, int* __restrict__ seg_b, int* __restrict__ seg_e) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -467,6 +546,21 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
         cuts.push_back(std::max(r1, r0 + 1));  // a single row always fits (< N events)
     }
 
+    // hop cap 2 with an on-chip bitset: sorted emission, no sort pass
+    const bool emit = hop_cap == 2 && smem;
+    const bool big_emit = bitset_bytes > 96 * 1024;  // one 1024-thread block per SM, else 256-thread blocks
+    int emit_grid = 1;
+    if (emit) {
+        int per = 1;
+        if (big_emit) {
+            cudaFuncSetAttribute(khop2_emit_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, khop2_emit_kernel<1024>, 1024, dyn);
+        } else {
+            cudaFuncSetAttribute(khop2_emit_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, khop2_emit_kernel<256>, 256, dyn);
+        }
+        emit_grid = num_sms() * std::max(per, 1);
+    }
     int walk_grid_cap = num_sms() * kWalkBlocksPerSM;
     for (std::size_t b = 0; b + 1 < cuts.size(); ++b) {
         const int r0 = cuts[b], r1 = cuts[b + 1], nr = r1 - r0;
@@ -508,11 +602,20 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
         F.ev = ev_raw;
         F.count = count + r0;
         cudaMemsetAsync(counter, 0, 16, st);
-        khop_expand_kernel<true><<<std::max(1, std::min(grid, nr)), kExpandThreads, dyn, st>>>(F);
+        const unsigned* ev_walk = ev_sorted;
+        if (emit) {
+            F.ev = ev_sorted;  // written in column order
+            if (big_emit)
+                khop2_emit_kernel<1024><<<std::max(1, std::min(emit_grid, nr)), 1024, dyn, st>>>(F);
+            else
+                khop2_emit_kernel<256><<<std::max(1, std::min(emit_grid, nr)), 256, dyn, st>>>(F);
+        } else {
+            khop_expand_kernel<true><<<std::max(1, std::min(grid, nr)), kExpandThreads, dyn, st>>>(F);
+        }
         count_launch();
         khop_segments_kernel<<<(nr + 255) / 256, 256, 0, st>>>(ev_off + r0, count + r0, nr, seg_b, seg_e);
         count_launch();
-        if (items > 0) {
+        if (items > 0 && !emit) {
             if ((e = cub::DeviceSegmentedSort::SortKeys(sort_tmp, sort_bytes, ev_raw, ev_sorted,
                                                         static_cast<int>(items), nr, seg_b, seg_e, st)) !=
                 cudaSuccess)
@@ -530,9 +633,9 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
         const int wgrid = static_cast<int>(
             std::min<long long>((nr + kWalkBlock / 32 - 1) / (kWalkBlock / 32), walk_grid_cap));
         if (hop_cap == 2)
-            khop_walk_kernel<true><<<wgrid, kWalkBlock, 0, st>>>(p, T, ev_sorted, seg_b, seg_e, r0, id_out, nr, wcounter);
+            khop_walk_kernel<true><<<wgrid, kWalkBlock, 0, st>>>(p, T, ev_walk, seg_b, seg_e, r0, id_out, nr, wcounter);
         else
-            khop_walk_kernel<false><<<wgrid, kWalkBlock, 0, st>>>(p, T, ev_sorted, seg_b, seg_e, r0, id_out, nr, wcounter);
+            khop_walk_kernel<false><<<wgrid, kWalkBlock, 0, st>>>(p, T, ev_walk, seg_b, seg_e, r0, id_out, nr, wcounter);
         count_launch();
         cudaFreeAsync(bm, st);
     }
