@@ -138,20 +138,24 @@ __global__ void __launch_bounds__(kExpandThreads) khop_expand_kernel(const KhopE
 // Hop cap 2 with the bitset on chip: the events are emitted already sorted.
 // Block per source row (rows from a queue): every neighbour's row is OR-ed
 // into the shared-memory bitset (warp per neighbour, coalesced 32-wide
-// chunks), the row itself and its neighbours are cleared again, and the
-// bitset is scanned in column order: warp w owns a contiguous word range,
-// counts its bits, the warps' counts are scanned, then each warp writes its
-// columns in ascending order (lane-parallel popc + warp scan) and zeroes
-// the words it read. No per-row sort and no second BFS.
+// chunks; a word that turns non-zero also sets its bit in a summary bitset,
+// one bit per word), the row itself and its neighbours are cleared again,
+// and the summary is walked in column order: thread t owns a contiguous run
+// of summary words, counts the columns under them, a block scan gives each
+// thread its output position, and it writes its columns ascending and zeroes
+// what it visited. Work per row is proportional to its events, not to N; no
+// per-row sort and no second BFS.
 template <int kThreads>
 __global__ void __launch_bounds__(kThreads) khop2_emit_kernel(const KhopExpand E) {
-    extern __shared__ unsigned bits[];
+    extern __shared__ unsigned bits[];  // [words] bitset, then [swords] summary
     __shared__ int s_row;
-    __shared__ int s_tot[kThreads / 32];
+    __shared__ int s_warp[kThreads / 32];
     constexpr int kWarps = kThreads / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int per = ((E.words + kWarps - 1) / kWarps + 31) & ~31;  // words per warp, multiple of 32
-    for (int w = tid; w < E.words; w += kThreads) bits[w] = 0u;
+    const int swords = (E.words + 31) >> 5;
+    unsigned* summ = bits + E.words;
+    const int spt = (swords + kThreads - 1) / kThreads;  // summary words per thread
+    for (int w = tid; w < E.words + swords; w += kThreads) bits[w] = 0u;
     __syncthreads();
     for (;;) {
         if (tid == 0) s_row = atomicAdd(E.counter, 1);
@@ -165,7 +169,8 @@ __global__ void __launch_bounds__(kThreads) khop2_emit_kernel(const KhopExpand E
             const long long ub = E.off[u], ue = E.off[u + 1];
             for (long long k = ub + lane; k < ue; k += 32) {
                 const int c = E.nbr[k];
-                atomicOr(&bits[c >> 5], 1u << (c & 31));
+                const int x = c >> 5;
+                if (atomicOr(&bits[x], 1u << (c & 31)) == 0u) atomicOr(&summ[x >> 5], 1u << (x & 31));
             }
         }
         __syncthreads();
@@ -175,41 +180,54 @@ __global__ void __launch_bounds__(kThreads) khop2_emit_kernel(const KhopExpand E
         }
         if (tid == 0) atomicAnd(&bits[i >> 5], ~(1u << (i & 31)));
         __syncthreads();
-        const int w0 = warp * per, w1 = min(E.words, w0 + per);
+        // count the columns under this thread's summary words
+        const int s0 = tid * spt, s1 = min(swords, s0 + spt);
         int cnt = 0;
-        for (int x = w0 + lane; x < w1; x += 32) cnt += __popc(bits[x]);
-        for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(kFull, cnt, d);
-        if (lane == 0) s_tot[warp] = cnt;
-        __syncthreads();
-        int base = 0;
-        for (int q = 0; q < warp; ++q) base += s_tot[q];
-        unsigned* dst = E.ev + (E.ev_off[r] - E.ev_base);
-        for (int x0 = w0; x0 < w1; x0 += 32) {
-            const int x = x0 + lane;
-            unsigned v = x < w1 ? bits[x] : 0u;
-            const int c = __popc(v);
-            int incl = c;
-            for (int d = 1; d < 32; d <<= 1) {
-                const int t = __shfl_up_sync(kFull, incl, d);
-                if (lane >= d) incl += t;
+        for (int sw = s0; sw < s1; ++sw) {
+            unsigned m = summ[sw];
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                cnt += __popc(bits[(sw << 5) + b]);
             }
-            int pos = base + incl - c;
-            if (v) {
+        }
+        // block exclusive scan of the counts
+        int incl = cnt;
+        for (int d = 1; d < 32; d <<= 1) {
+            const int t = __shfl_up_sync(kFull, incl, d);
+            if (lane >= d) incl += t;
+        }
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            int v = lane < kWarps ? s_warp[lane] : 0;
+            for (int d = 1; d < 32; d <<= 1) {
+                const int t = __shfl_up_sync(kFull, v, d);
+                if (lane >= d) v += t;
+            }
+            if (lane < kWarps) s_warp[lane] = v;  // inclusive warp totals
+        }
+        __syncthreads();
+        int pos = incl - cnt + (warp ? s_warp[warp - 1] : 0);
+        unsigned* dst = E.ev + (E.ev_off[r] - E.ev_base);
+        for (int sw = s0; sw < s1; ++sw) {
+            unsigned m = summ[sw];
+            if (!m) continue;
+            summ[sw] = 0u;
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                const int x = (sw << 5) + b;
+                unsigned v = bits[x];
                 bits[x] = 0u;
                 const unsigned col0 = static_cast<unsigned>(x) << 5;
                 while (v) {
-                    const int b = __ffs(v) - 1;
-                    dst[pos++] = ((col0 + b) << 3) | 2u;
+                    dst[pos++] = ((col0 + (__ffs(v) - 1)) << 3) | 2u;
                     v &= v - 1;
                 }
             }
-            base += __shfl_sync(kFull, incl, 31);
         }
-        if (tid == 0) {
-            int tot = 0;
-            for (int q = 0; q < kWarps; ++q) tot += s_tot[q];
-            E.count[r] = tot;
-        }
+        if (tid == 0) E.count[r] = s_warp[kWarps - 1];
         __syncthreads();
     }
 }
@@ -547,17 +565,19 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
     }
 
     // hop cap 2 with an on-chip bitset: sorted emission, no sort pass
-    const bool emit = hop_cap == 2 && smem;
-    const bool big_emit = bitset_bytes > 96 * 1024;  // one 1024-thread block per SM, else 256-thread blocks
+    const std::size_t emit_bytes = bitset_bytes + static_cast<std::size_t>((words + 31) / 32) * 4;
+    const bool emit = hop_cap == 2 && emit_bytes <= kSmemBitsetBytes;
+    const bool big_emit = emit_bytes > 96 * 1024;  // one 1024-thread block per SM, else 256-thread blocks
+    const int edyn = static_cast<int>(emit_bytes);
     int emit_grid = 1;
     if (emit) {
         int per = 1;
         if (big_emit) {
-            cudaFuncSetAttribute(khop2_emit_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, khop2_emit_kernel<1024>, 1024, dyn);
+            cudaFuncSetAttribute(khop2_emit_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, edyn);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, khop2_emit_kernel<1024>, 1024, edyn);
         } else {
-            cudaFuncSetAttribute(khop2_emit_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, khop2_emit_kernel<256>, 256, dyn);
+            cudaFuncSetAttribute(khop2_emit_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, edyn);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, khop2_emit_kernel<256>, 256, edyn);
         }
         emit_grid = num_sms() * std::max(per, 1);
     }
@@ -606,9 +626,9 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
         if (emit) {
             F.ev = ev_sorted;  // written in column order
             if (big_emit)
-                khop2_emit_kernel<1024><<<std::max(1, std::min(emit_grid, nr)), 1024, dyn, st>>>(F);
+                khop2_emit_kernel<1024><<<std::max(1, std::min(emit_grid, nr)), 1024, edyn, st>>>(F);
             else
-                khop2_emit_kernel<256><<<std::max(1, std::min(emit_grid, nr)), 256, dyn, st>>>(F);
+                khop2_emit_kernel<256><<<std::max(1, std::min(emit_grid, nr)), 256, edyn, st>>>(F);
         } else {
             khop_expand_kernel<true><<<std::max(1, std::min(grid, nr)), kExpandThreads, dyn, st>>>(F);
         }
