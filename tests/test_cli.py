@@ -49,6 +49,10 @@ def test_invalid_parameters_exit_2():
     assert run("bench", "--sizes", "10,5")[0] == 2
     code, out, err = run("cluster", k, "--sigma", "-1")
     assert "sigma must be positive" in err
+    for bad in ("0", "8"):  # --hop-cap (k-hop extension, not a reference flag)
+        code, out, err = run("cluster", k, "--sigma", "1", "--hop-cap", bad)
+        assert code == 2 and "hop-cap must be in 1..7" in err
+    assert run("sweep", k, "--hop-cap", "x")[0] == 2
 
 
 def test_io_failures_exit_1(tmp_path):
@@ -241,3 +245,21 @@ def test_config2_small_graph_sweeps_match_oracle(tmp_path, name):
         assert code == 0, err
         a, r = O.run_cluster(path, None, sigma)
         assert a_csv.read_text() == a and out == r
+
+
+@pytest.mark.gpu
+def test_cluster_hop_cap_extension(tmp_path):
+    """--hop-cap 2 (the opt-in k-hop distance, not a reference feature): the
+    assignment equals GGD over the k-hop oracle's field; --hop-cap 1 is the
+    README golden again."""
+    out_csv = tmp_path / "a.csv"
+    code, out, err = run("cluster", H.KARATE_EDGES, "--sigma", "3", "--hop-cap", "2", "--out", out_csv)
+    assert code == 0, err
+    g, names, _, _ = H.karate()
+    v = O.potentials_khop(g.offsets, g.nbr, g.wt, g.W, 3.0, 2, workers=2)
+    center, ci, k = O.resolve_centers(O.build_successors(g.offsets, g.nbr, v))
+    want = "node,center,cluster\n" + "".join(f"{names[i]},{names[center[i]]},{ci[i]}\n" for i in range(g.n))
+    assert out_csv.read_text() == want
+    code, out, err = run("cluster", H.KARATE_EDGES, "--labels", H.KARATE_LABELS, "--sigma", "5", "--hop-cap", "1",
+                         "--out", tmp_path / "b.csv")
+    assert code == 0 and out.splitlines()[1] == README_ROW
