@@ -8,17 +8,23 @@
 // only as the checker or the timed CPU baseline — never as the product path.
 //
 // Every function cites the reference file:line it restates (paths relative to
-// the reference's proj/ directory). The reference itself cannot be compiled
-// in this image (Eigen3, CLI11, doctest and nlohmann/json are absent, see
-// DESIGN.md), so the restatement replaces Eigen::VectorXd by std::vector and
-// restates the one third-party arithmetic the path depends on, Eigen 3.4's
-// vectorised exp (pexp_double on SSE2 Packet2d), lane by lane.
+// the reference's proj/ directory). The reference's build needs Eigen3, which
+// this image lacks, so the restatement replaces Eigen::VectorXd by
+// std::vector and restates the one third-party arithmetic the path depends
+// on, Eigen 3.4's vectorised exp (pexp_double on SSE2 Packet2d), lane by lane.
 //
-// Pinning: labels, centers, reports and the sweep mutation line are pinned to
-// the reference's published goldens (README.md:58-59, :69; ggd_test.cpp:144-156;
-// sweep_test.cpp:72-89, :144-153; metrics_test.cpp:65-97). Potential BITS are
-// pinned only to this restatement of Eigen's pexp ("potential bits: parity
-// unpinned against an Eigen-built reference" — no Eigen source here).
+// Pinning: tests/test_ref_pin.py checks this file bit for bit against the
+// reference's OWN sources compiled in place (oracle/_ref, Makefile target
+// `ref`, Eigen replaced by the restated subset in eigen_shim/): potentials,
+// GGD, ingestion, metrics, sweep CSVs, grids. tests/test_oracle.py checks it
+// against the reference's published goldens (README.md:58-59, :69;
+// ggd_test.cpp:144-156; sweep_test.cpp:72-89, :144-153; metrics_test.cpp:65-97).
+// Still unpinned: the exp BITS of an Eigen-built binary (no Eigen source here;
+// both this file and eigen_shim restate Eigen 3.4's pexp_double).
+//
+// The k-hop distance extension (fill_khop) is NOT a reference feature; at hop
+// cap 1 it is the reference's distance, and it is checked against a direct
+// restatement of its definition in tests/test_oracle.py.
 //
 // Build: g++ -O2 -std=c++20 -ffp-contract=off (no -march: SSE2 scalar double,
 // no FMA, exactly the reference's default Release arithmetic).
