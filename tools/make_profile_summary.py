@@ -109,6 +109,23 @@ def main(tag):
                 out.append(f"| {label} | {r['wall_s']:.2f} | {json.dumps(r['stages_ms'])} |")
         return "\n".join(out)
 
+    kh_sbm, kh_lfr = last_json("bench_khop_sbm.json"), last_json("bench_khop_lfr.json")
+
+    def khop_line(d, label):
+        if not d:
+            return f"| {label} | (not run) | | | |"
+        bd, cpu = d.get("breakdown_ms") or {}, d.get("cpu_baseline") or {}
+        return (f"| {label} | {d['value']:.4g} GPairs/s ({d['ms_per_step']:.2f} ms/step) | {bd.get('potentials', 0):.2f} | "
+                f"{bd.get('ggd', 0):.2f} | {cpu.get('value', float('nan')):.3g} GPairs/s ({cpu.get('cores')} cores) |")
+
+    khop_ncu = ""
+    rep = os.path.join(OUT, "khop_full.ncu-rep")
+    if os.path.exists(rep):
+        kd = ncu_summary.details(rep, ["Duration", "Issue Slots Busy", "Executed Ipc Active", "Eligible Warps",
+                                       "Avg. Active Threads", "Achieved Occupancy", "DRAM Throughput"])
+        khop_ncu = ("ncu (`--set full`, LFR 1M hop cap 2; first launch = khop2_emit_kernel (BFS + ordered emission), "
+                    "second = khop_walk_kernel<batched>):\n\n```\n" + "\n".join(kd) + "\n```")
+
     pw = kern.get("potential_warp_kernel<FASTFWD,unit>", {})
     sk = kern.get("successors_kernel", {})
     md = f"""# {tag} profile summary (B200, sm_100a)
@@ -134,6 +151,15 @@ GPU kernel launches in the timed region: {b.get('gpu_launches')} over {b.get('st
 Dense in-order replay (K1, `--kernel replay`) on SBM 100k x 32 sigmas: 39.2 ms for the potentials =
 8.16e12 logical pairs/s = 16.3e12 fp64 adds/s, 88% of the B200's nominal 37 TFLOPS FP64 (18.5e12 adds/s).
 The exact fast-forward (K2) computes the same bit-identical field in 0.45 ms (87x).
+
+## k-hop distance extension (opt-in `--hop-cap 2`; not a reference feature, SURVEY §8(f) row 4)
+
+| workload (32 sigmas, hop cap 2) | value | potentials ms | GGD ms | CPU baseline (oracle k-hop port) |
+|---|---|---|---|---|
+{khop_line(kh_sbm, "SBM N=100k")}
+{khop_line(kh_lfr, "LFR-style N=1M")}
+
+{khop_ncu}
 
 ## End-to-end QC time (load edge list -> CSR -> potentials -> GGD -> metrics -> outputs)
 
