@@ -146,12 +146,12 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sel)}
 
 
-def recorded_traffic(kernel_key):
-    """DRAM bytes per launch of a kernel from the committed ncu capture
-    (profiles/traffic.json), or None."""
+def recorded_traffic(kernel_key, field="dram_bytes"):
+    """A per-launch ncu figure of a kernel from the committed capture
+    (profiles/traffic.json): DRAM bytes by default, or None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
-        return json.load(open(p))[kernel_key]["dram_bytes"]
+        return json.load(open(p))[kernel_key][field]
     except (OSError, KeyError, ValueError):
         return None
 
@@ -424,7 +424,14 @@ def run_native(args):
                                     "k-hop pipeline (khop_expand x2 + segmented sort + khop_walk_kernel)"),
                          "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
                          "note": "algorithmic bytes = 8(rows+1) + 4*nnz + 8*rows*S; the exact fast-forward is "
-                                 "issue-bound (fp64/int chain arithmetic), see DESIGN.md"},
+                                 "issue-bound (fp64/int chain arithmetic), see DESIGN.md",
+                         "binding": ({"resource": "instruction issue",
+                                      "issue_slots_busy_pct": recorded_traffic("potential_warp_kernel<FASTFWD,unit>",
+                                                                               "issue_active_pct"),
+                                      "warp_instructions": recorded_traffic("potential_warp_kernel<FASTFWD,unit>",
+                                                                            "inst_executed"),
+                                      "source": "profiles/traffic.json (ncu --set full)"}
+                                     if args.hop_cap == 1 else None)},
             "clocks": clocks, "gpu_launches": gpu_launches,
             "e2e": e2e, "cpu_baseline": cpu,
         }
