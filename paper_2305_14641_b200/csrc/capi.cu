@@ -538,7 +538,7 @@ gqc_status gqc_resolve_centers(int32_t n, const int32_t* succ, int32_t* center, 
 }
 
 #ifndef GQC_GGD_CHUNK
-#define GQC_GGD_CHUNK 16
+#define GQC_GGD_CHUNK 0
 #endif
 // sigmas per GGD pass of the host pipeline: each pass's labels go down while
 // the next pass computes, so the last pass's download is the exposed tail
@@ -631,7 +631,17 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
         int* dnc = C.nc.get<int>(n_sigma);
         const std::size_t wsb = labels_workspace_bytes(n, n_sigma);
         void* ws = C.ws.get<char>(wsb);
-        const int chunk = n_sigma > kGgdChunk ? kGgdChunk : n_sigma;
+        // GGD chunk boundaries. The label downloads are bound by the D2H link
+        // and can only start after the first chunk, so chunks grow: the first
+        // is small (downloads start early), later ones amortise launches
+        // (S = 32: 4, 8, 8, 12 sigmas). GQC_GGD_CHUNK > 0 forces equal chunks.
+        std::vector<int> cuts{0};
+        if (kGgdChunk > 0) {
+            for (int s0 = kGgdChunk; s0 < n_sigma; s0 += kGgdChunk) cuts.push_back(s0);
+        } else if (n_sigma >= 16) {
+            for (int f : {1, 3, 5}) cuts.push_back((n_sigma * f + 7) / 8);
+        }
+        cuts.push_back(n_sigma);
         // labels of a chunk go down while the next chunk computes; into
         // pageable buffers every copy blocks the host, so then all chunks are
         // launched first and the copies queued after them
@@ -650,8 +660,8 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
             cuda_check(cudaMemcpyAsync(nc_stage + s0, dnc + s0, Sc * sizeof(int), cudaMemcpyDeviceToHost, cs),
                        "copy counts");
         };
-        for (int s0 = 0; s0 < n_sigma; s0 += chunk) {
-            const int Sc = std::min(chunk, n_sigma - s0);
+        for (std::size_t q = 0; q + 1 < cuts.size(); ++q) {
+            const int s0 = cuts[q], Sc = cuts[q + 1] - cuts[q];
             const std::size_t o = static_cast<std::size_t>(s0) * n;
             cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, s0, Sc, 0, n, ds + o, 1, n, nnz, C.pool, st), "successor kernel");
             cuda_check(launch_chase(n, Sc, ds + o, dc + o, st, ws), "chase kernel");
@@ -670,7 +680,7 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
             cuda_check(cudaStreamWaitEvent(cs, C.ev[9], 0), "wait");
         }
         if (!overlap)
-            for (int s0 = 0; s0 < n_sigma; s0 += chunk) download(s0, std::min(chunk, n_sigma - s0));
+            for (std::size_t q = 0; q + 1 < cuts.size(); ++q) download(cuts[q], cuts[q + 1] - cuts[q]);
         if (v_out && !v_early)
             cuda_check(cudaMemcpyAsync(v_out, v_src, cells * sizeof(double), cudaMemcpyDeviceToHost, cs), "copy V");
         cuda_check(cudaEventRecord(C.ev[8], cs), "event");
