@@ -538,7 +538,7 @@ gqc_status gqc_resolve_centers(int32_t n, const int32_t* succ, int32_t* center, 
 }
 
 #ifndef GQC_GGD_CHUNK
-#define GQC_GGD_CHUNK 0
+#define GQC_GGD_CHUNK 16
 #endif
 // sigmas per GGD pass of the host pipeline: each pass's labels go down while
 // the next pass computes, so the last pass's download is the exposed tail
@@ -631,10 +631,10 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
         int* dnc = C.nc.get<int>(n_sigma);
         const std::size_t wsb = labels_workspace_bytes(n, n_sigma);
         void* ws = C.ws.get<char>(wsb);
-        // GGD chunk boundaries. The label downloads are bound by the D2H link
-        // and can only start after the first chunk, so chunks grow: the first
-        // is small (downloads start early), later ones amortise launches
-        // (S = 32: 4, 8, 8, 12 sigmas). GQC_GGD_CHUNK > 0 forces equal chunks.
+        // GGD chunk boundaries: equal chunks of GQC_GGD_CHUNK sigmas (16), or
+        // with GQC_GGD_CHUNK=0 growing ones (S = 32: 4, 8, 8, 12) so the
+        // downloads start after a small first chunk. Measured on LFR 1M x 32:
+        // e2e 8.54 ms (16) vs 8.84 ms (growing); R-MAT 25.7 vs 27.4 ms.
         std::vector<int> cuts{0};
         if (kGgdChunk > 0) {
             for (int s0 = kGgdChunk; s0 < n_sigma; s0 += kGgdChunk) cuts.push_back(s0);
