@@ -375,6 +375,37 @@ gqc_csr upload_csr(DeviceCtx& C, const gqc_csr* g, cudaStream_t st, const double
     return d;
 }
 
+
+// Degree-class order of a field for the GGD argmin fast path (kernels.cu,
+// launch_class_order). Verified per sigma on the field, so it is exact for
+// any input; GQC_CLASS_ORDER=0 disables it (A/B measurements).
+struct ClassOrderScope {
+    ClassOrder co;
+    void* mem = nullptr;
+    cudaStream_t st = nullptr;
+    ClassOrderScope() = default;
+    ClassOrderScope(const ClassOrderScope&) = delete;
+    ClassOrderScope& operator=(const ClassOrderScope&) = delete;
+    ~ClassOrderScope() {
+        if (mem) cudaFreeAsync(mem, st);
+    }
+    const ClassOrder* get() const { return co.dir ? &co : nullptr; }
+};
+
+bool class_order_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("GQC_CLASS_ORDER");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
+void make_class_order(DeviceCtx& C, int n, const std::int64_t* off, long long nnz, const double* v, int ld, int S,
+                      cudaStream_t st, ClassOrderScope& out) {
+    if (!class_order_enabled()) return;
+    out.st = st;
+    cuda_check(launch_class_order(n, off, nnz, v, ld, S, C.pool, st, &out.co, &out.mem), "class order");
+}
 }  // namespace
 
 void count_launch(int k) { t_launches += k; }
@@ -660,10 +691,14 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
             cuda_check(cudaMemcpyAsync(nc_stage + s0, dnc + s0, Sc * sizeof(int), cudaMemcpyDeviceToHost, cs),
                        "copy counts");
         };
+        ClassOrderScope order;
+        make_class_order(C, n, d.offsets, nnz, v_nm, n_sigma, n_sigma, st, order);
         for (std::size_t q = 0; q + 1 < cuts.size(); ++q) {
             const int s0 = cuts[q], Sc = cuts[q + 1] - cuts[q];
             const std::size_t o = static_cast<std::size_t>(s0) * n;
-            cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, s0, Sc, 0, n, ds + o, 1, n, nnz, C.pool, st), "successor kernel");
+            cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, s0, Sc, 0, n, ds + o, 1, n, nnz, C.pool, st,
+                                         order.get()),
+                       "successor kernel");
             cuda_check(launch_chase(n, Sc, ds + o, dc + o, st, ws), "chase kernel");
             cuda_check(launch_labels(n, Sc, dc + o, dci + o, dnc + s0, ws, wsb, st, true), "label kernels");
             tr.mark("ggd_chunk");
@@ -746,7 +781,11 @@ gqc_status gqc_dev_ggd(const gqc_csr* g, const double* v, int32_t n_sigma, int32
         auto st = static_cast<cudaStream_t>(stream);
         DeviceCtx& C = ctx(st, g->offsets);
         int* s = succ ? succ : center;  // the chase runs in place on center
-        cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, 0, g->n, s, 1, g->n, g->nnz, C.pool, st), "successor kernel");
+        ClassOrderScope order;
+        make_class_order(C, g->n, g->offsets, g->nnz, v, n_sigma, n_sigma, st, order);
+        cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, 0, g->n, s, 1, g->n, g->nnz, C.pool,
+                                     st, order.get()),
+                   "successor kernel");
         cuda_check(launch_chase(g->n, n_sigma, s, center, st, workspace), "chase kernel");
         cuda_check(launch_labels(g->n, n_sigma, center, cluster_index, num_clusters, workspace, workspace_bytes, st, true),
                    "label kernels");
@@ -760,9 +799,12 @@ gqc_status gqc_dev_successors(const gqc_csr* g, const double* v, int32_t n_sigma
         if (n_sigma < 1) fail(GQC_EINVAL, "sigma grid is empty");
         if (row_begin < 0 || row_end > g->n || row_begin > row_end) fail(GQC_ERANGE, "row range out of range");
         if (!v || (!succ_rows && row_end > row_begin)) fail(GQC_EINVAL, "null buffer");
-        DeviceCtx& C = ctx(static_cast<cudaStream_t>(stream), g->offsets);
+        auto st = static_cast<cudaStream_t>(stream);
+        DeviceCtx& C = ctx(st, g->offsets);
+        ClassOrderScope order;
+        make_class_order(C, g->n, g->offsets, g->nnz, v, n_sigma, n_sigma, st, order);
         cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, row_begin, row_end, succ_rows,
-                                     n_sigma, 1, g->nnz, C.pool, static_cast<cudaStream_t>(stream)),
+                                     n_sigma, 1, g->nnz, C.pool, st, order.get()),
                    "successor kernel");
     });
 }

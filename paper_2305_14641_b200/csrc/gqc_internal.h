@@ -58,14 +58,30 @@ struct PotentialLaunch {
 // Stream-ordered scratch comes from `pool` (a cudaMemPool_t that keeps its
 // memory, so per-call scratch costs no driver allocation).
 int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* stream);
+// Degree-class order of a potential field (unit-weight fast path of the GGD
+// argmin, see kernels.cu): cls[i] = rank of node i's degree among the
+// distinct degrees, dir[s] = +1 / -1 when, for sigma s, every node of a lower
+// class has a strictly smaller / larger potential than every node of a higher
+// class (verified on the field itself, not assumed), 0 otherwise.
+struct ClassOrder {
+    const std::int32_t* cls = nullptr;
+    const signed char* dir = nullptr;  // indexed by the sigma column of V
+};
+// Builds the order for V (node-major, leading dimension ld, n_sigma columns)
+// into pool scratch *mem (release with cudaFreeAsync(*mem, stream) after the
+// successor launches that use it).
+int launch_class_order(std::int32_t n, const std::int64_t* offsets, long long nnz, const double* v, std::int32_t ld,
+                       std::int32_t n_sigma, void* pool, void* stream, ClassOrder* out, void** mem);
 // GGD argmin for rows [row_begin, row_end) and the sigma columns
 // [s0, s0 + n_sigma) of a node-major V with leading dimension ld. Element
 // (row r of the range, sigma q) goes to out[r * out_row + q * out_col]
 // (sigma-major: out_row = 1, out_col = n; node-major shard: out_row = ld, out_col = 1).
+// co (optional): the field's class order; sigmas with dir != 0 take the
+// fast path (only best-class neighbours' potentials are gathered).
 int launch_successors(std::int32_t n, const std::int64_t* offsets, const std::int32_t* nbr, const double* v,
                       std::int32_t ld, std::int32_t s0, std::int32_t n_sigma, std::int32_t row_begin,
                       std::int32_t row_end, std::int32_t* out, long long out_row, long long out_col, long long nnz,
-                      void* pool, void* stream);
+                      void* pool, void* stream, const ClassOrder* co = nullptr);
 int launch_transpose_i32(const std::int32_t* in, std::int32_t n, std::int32_t n_sigma, std::int32_t* out, void* stream);
 // labels_workspace (optional): launch_labels' workspace; the chase then writes
 // the center flags there and launch_labels must be called with flags_ready.

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <map>
 #include <utility>
 
@@ -600,10 +601,14 @@ struct SuccOut {
 constexpr int kSuccUnroll = GQC_SUCC_UNROLL;    // gathers in flight per thread (light rows)
 constexpr int kHeavyUnroll = GQC_HEAVY_UNROLL;  // gathers in flight per warp (heavy rows)
 
+__device__ __forceinline__ bool lex_less(double va, int ia, double vb, int ib) {
+    return va < vb || (va == vb && ia < ib);
+}
+
 __global__ void __launch_bounds__(kBlock) successors_kernel(const long long* __restrict__ off,
                                                             const int* __restrict__ nbr,
                                                             const double* __restrict__ v, int ld, int s0, int Sc,
-                                                            int row_begin, int rows, SuccOut O) {
+                                                            int row_begin, int rows, SuccOut O, ClassOrder co) {
     // rows * Sc < 2^31 (launch_successors checks): 32-bit index math
     const unsigned tid = blockIdx.x * static_cast<unsigned>(kBlock) + threadIdx.x;
     const unsigned r = tid / static_cast<unsigned>(Sc);
@@ -618,6 +623,35 @@ __global__ void __launch_bounds__(kBlock) successors_kernel(const long long* __r
     const long long kend = off[i + 1];
     if (kend - k > kHeavyDegree) return;  // heavy rows: successors_heavy_kernel
     int best = i;
+    const int dir = co.dir ? co.dir[s] : 0;
+    if (dir != 0) {
+        // Degree-class fast path (dir verified for this sigma by
+        // launch_class_order): a node of a better class beats every node of a
+        // worse one, so the lexicographic (v, id) minimum lies in the best
+        // class present in the closed neighbourhood; only that class's
+        // potentials are gathered (the class ids are a 4 B, L2-resident gather).
+        const int ci = __ldg(co.cls + i);
+        int bc = ci;
+        for (long long kk = k; kk < kend; ++kk) {
+            const int c = __ldg(co.cls + __ldg(nbr + kk));
+            bc = dir > 0 ? min(bc, c) : max(bc, c);
+        }
+        if (bc != ci) {
+            best = 0x7fffffff;
+            vb = __longlong_as_double(0x7ff0000000000000ll);
+        }
+        for (; k < kend; ++k) {
+            const int j = __ldg(nbr + k);
+            if (__ldg(co.cls + j) != bc) continue;
+            const double vj = __ldg(v + static_cast<long long>(j) * ld + s);
+            if (lex_less(vj, j, vb, best)) {
+                best = j;
+                vb = vj;
+            }
+        }
+        O.out[static_cast<long long>(r) * O.out_row + q * O.out_col] = best;
+        return;
+    }
     // kSuccUnroll independent gathers in flight, compared in ascending k
     for (; k + kSuccUnroll <= kend; k += kSuccUnroll) {
         int j[kSuccUnroll];
@@ -676,10 +710,6 @@ __global__ void mark_heavy_kernel(const long long* __restrict__ off, int row_beg
         multi[atomicAdd(&counts[2], 1)] = HeavyRow{i, slot0, nseg};
     }
     for (int q = 0; q < nseg; ++q) items[base + q] = HeavyItem{i, q, nseg > 1 ? slot0 + q : -1};
-}
-
-__device__ __forceinline__ bool lex_less(double va, int ia, double vb, int ib) {
-    return va < vb || (va == vb && ia < ib);
 }
 
 __global__ void __launch_bounds__(kBlock) successors_heavy_kernel(const long long* __restrict__ off,
@@ -1045,9 +1075,166 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
     return e;
 }
 
+namespace {
+
+// ---------------------------------------------------------------------------
+// Degree-class order (ClassOrder, gqc_internal.h). On a unit-weight graph a
+// row's potential is mathematically a Moebius function of its degree d
+// (num and den are affine in d, potential.cpp:18-37), hence monotone in d;
+// rounding noise separates equal-degree nodes only. Whether the field at
+// hand really orders its degree classes strictly is VERIFIED per sigma:
+// nodes are sorted by degree, each class's [min, max] potential is reduced,
+// and consecutive classes must not overlap (in one direction). A sigma that
+// fails (weighted graphs, k-hop fields, saturated regimes) keeps the plain
+// argmin. Potentials are >= +0, so their bit patterns order like the values.
+// ---------------------------------------------------------------------------
+__global__ void class_key_kernel(const long long* __restrict__ off, int n, int* __restrict__ key,
+                                 int* __restrict__ id) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        key[i] = static_cast<int>(off[i + 1] - off[i]);
+        id[i] = i;
+    }
+}
+
+__global__ void class_flag_kernel(const int* __restrict__ sdeg, int n, int* __restrict__ flag) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) flag[k] = (k == 0 || sdeg[k] != sdeg[k - 1]) ? 1 : 0;
+}
+
+// cls[node] = class index (inclusive scan - 1); clear the min / max tables
+__global__ void class_scatter_kernel(const int* __restrict__ sid, const int* __restrict__ cidx, int n, int S,
+                                     int* __restrict__ cls, unsigned long long* __restrict__ mn,
+                                     unsigned long long* __restrict__ mx) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) cls[sid[k]] = cidx[k] - 1;
+    const int C = cidx[n - 1];
+    for (long long t = k; t < static_cast<long long>(C) * S; t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        mn[t] = ~0ull;
+        mx[t] = 0ull;
+    }
+}
+
+// warp per run of kClassRun sorted positions, lane = sigma: running min / max
+// of the class, flushed with 64-bit atomics when the class changes
+constexpr int kClassRun = 64;
+__global__ void class_minmax_kernel(const int* __restrict__ sid, const int* __restrict__ cls,
+                                    const double* __restrict__ v, int ld, int S, int n,
+                                    unsigned long long* __restrict__ mn, unsigned long long* __restrict__ mx) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int k0 = w * kClassRun;
+    if (k0 >= n) return;
+    const int k1 = min(n, k0 + kClassRun);
+    for (int sb = 0; sb < S; sb += 32) {
+        const int s = sb + lane;
+        int cur = -1;
+        unsigned long long lo = ~0ull, hi = 0ull;
+        for (int k = k0; k < k1; ++k) {
+            const int i = __ldg(sid + k);
+            const int c = __ldg(cls + i);
+            if (c != cur) {
+                if (cur >= 0 && s < S) {
+                    atomicMin(mn + static_cast<long long>(cur) * S + s, lo);
+                    atomicMax(mx + static_cast<long long>(cur) * S + s, hi);
+                }
+                cur = c;
+                lo = ~0ull;
+                hi = 0ull;
+            }
+            if (s < S) {
+                const unsigned long long b =
+                    static_cast<unsigned long long>(__double_as_longlong(__ldg(v + static_cast<long long>(i) * ld + s)));
+                lo = min(lo, b);
+                hi = max(hi, b);
+            }
+        }
+        if (s < S) {
+            atomicMin(mn + static_cast<long long>(cur) * S + s, lo);
+            atomicMax(mx + static_cast<long long>(cur) * S + s, hi);
+        }
+    }
+}
+
+// viol[s] bit 0: some consecutive classes not strictly ascending; bit 1: not
+// strictly descending
+__global__ void class_check_kernel(const unsigned long long* __restrict__ mn, const unsigned long long* __restrict__ mx,
+                                   const int* __restrict__ cidx, int n, int S, int* __restrict__ viol) {
+    const long long pairs = static_cast<long long>(cidx[n - 1] - 1) * S;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < pairs;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long c = t / S;
+        const int s = static_cast<int>(t - c * S);
+        const long long a = c * S + s, b = (c + 1) * S + s;
+        int f = 0;
+        if (!(mx[a] < mn[b])) f |= 1;
+        if (!(mn[a] > mx[b])) f |= 2;
+        if (f) atomicOr(viol + s, f);
+    }
+}
+
+__global__ void class_dir_kernel(const int* __restrict__ viol, int S, signed char* __restrict__ dir) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < S) dir[s] = !(viol[s] & 1) ? 1 : (!(viol[s] & 2) ? -1 : 0);
+}
+
+}  // namespace
+
+int launch_class_order(int n, const std::int64_t* offsets, long long nnz, const double* v, int ld, int S, void* pool_,
+                       void* stream, ClassOrder* out, void** mem) {
+    auto st = static_cast<cudaStream_t>(stream);
+    auto pool = static_cast<cudaMemPool_t>(pool_);
+    *mem = nullptr;
+    if (n < 1 || S < 1) return cudaSuccess;
+    // distinct degrees d_1 < ... < d_C sum to at most nnz: C <= sqrt(2 nnz) + 1
+    const long long cmax = std::min<long long>(n, static_cast<long long>(std::sqrt(2.0 * static_cast<double>(nnz))) + 2);
+    int end_bit = 1;
+    while (end_bit < 31 && (1ll << end_bit) <= nnz) ++end_bit;
+    std::size_t sort_bytes = 0, scan_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, static_cast<const int*>(nullptr), static_cast<int*>(nullptr),
+                                    static_cast<const int*>(nullptr), static_cast<int*>(nullptr), n, 0, end_bit);
+    cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, static_cast<const int*>(nullptr), static_cast<int*>(nullptr), n);
+    auto al = [](std::size_t b) { return (b + 255) & ~static_cast<std::size_t>(255); };
+    const std::size_t b_n = al(static_cast<std::size_t>(n) * sizeof(int));
+    const std::size_t b_t = al(static_cast<std::size_t>(cmax) * S * sizeof(unsigned long long));
+    const std::size_t b_s = al(static_cast<std::size_t>(S) * sizeof(int));
+    const std::size_t total = 6 * b_n + 2 * b_t + 2 * b_s + al(std::max(sort_bytes, scan_bytes));
+    cudaError_t e = cudaMallocFromPoolAsync(mem, total, pool, st);
+    if (e != cudaSuccess) return e;
+    char* m = static_cast<char*>(*mem);
+    int* key = reinterpret_cast<int*>(m);
+    int* id = reinterpret_cast<int*>(m + b_n);
+    int* sdeg = reinterpret_cast<int*>(m + 2 * b_n);
+    int* sid = reinterpret_cast<int*>(m + 3 * b_n);
+    int* cidx = reinterpret_cast<int*>(m + 4 * b_n);
+    int* cls = reinterpret_cast<int*>(m + 5 * b_n);
+    auto* mn = reinterpret_cast<unsigned long long*>(m + 6 * b_n);
+    auto* mx = reinterpret_cast<unsigned long long*>(m + 6 * b_n + b_t);
+    int* viol = reinterpret_cast<int*>(m + 6 * b_n + 2 * b_t);
+    auto* dir = reinterpret_cast<signed char*>(m + 6 * b_n + 2 * b_t + b_s);
+    void* tmp = m + 6 * b_n + 2 * b_t + 2 * b_s;
+    auto off = reinterpret_cast<const long long*>(offsets);
+    const int g = grid_for(n);
+    class_key_kernel<<<g, kBlock, 0, st>>>(off, n, key, id);
+    if ((e = cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, key, sdeg, id, sid, n, 0, end_bit, st)) != cudaSuccess)
+        return e;
+    class_flag_kernel<<<g, kBlock, 0, st>>>(sdeg, n, key);
+    if ((e = cub::DeviceScan::InclusiveSum(tmp, scan_bytes, key, cidx, n, st)) != cudaSuccess) return e;
+    class_scatter_kernel<<<g, kBlock, 0, st>>>(sid, cidx, n, S, cls, mn, mx);
+    const long long warps = (n + kClassRun - 1) / kClassRun;
+    class_minmax_kernel<<<static_cast<unsigned>((warps * 32 + kBlock - 1) / kBlock), kBlock, 0, st>>>(sid, cls, v, ld,
+                                                                                                     S, n, mn, mx);
+    cudaMemsetAsync(viol, 0, S * sizeof(int), st);
+    class_check_kernel<<<512, kBlock, 0, st>>>(mn, mx, cidx, n, S, viol);
+    class_dir_kernel<<<(S + kBlock - 1) / kBlock, kBlock, 0, st>>>(viol, S, dir);
+    count_launch(10);
+    out->cls = cls;
+    out->dir = dir;
+    return cudaGetLastError();
+}
+
 int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nbr, const double* v, int ld, int s0,
                       int n_sigma, int row_begin, int row_end, std::int32_t* out, long long out_row, long long out_col,
-                      long long nnz, void* pool, void* stream) {
+                      long long nnz, void* pool, void* stream, const ClassOrder* co) {
     (void)n;
     auto st = static_cast<cudaStream_t>(stream);
     auto off = reinterpret_cast<const long long*>(offsets);
@@ -1088,7 +1275,8 @@ int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nb
         const SuccOut O{out + c0 * out_col, out_row, out_col};
         const long long threads = static_cast<long long>(rows) * Sc;
         if (threads >= (1ll << 31) - kBlock) return cudaErrorInvalidValue;  // 32-bit thread ids
-        successors_kernel<<<grid_for(threads), kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, rows, O);
+        successors_kernel<<<grid_for(threads), kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, rows, O,
+                                                                 co ? *co : ClassOrder{});
         successors_heavy_kernel<<<num_sms * 8, kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, items, counts,
                                                                  part_v, part_i, O);
         successors_combine_kernel<<<num_sms * 2, kBlock, 0, st>>>(multi, counts, part_v, part_i, Sc, row_begin, O);

@@ -529,3 +529,50 @@ def test_device_binding_follows_stream_and_option():
     assert torch.equal(out.view(torch.int64), out2.view(torch.int64))
     with pytest.raises(ValueError):
         N.set_device(torch.cuda.device_count())
+
+
+def test_degree_class_order_fast_path_matches_plain_argmin():
+    """GGD argmin fast path (launch_class_order): on unit-weight graphs the
+    degree classes order the potentials for most sigmas and only the best
+    class is gathered. Same labels as the plain argmin (GQC_CLASS_ORDER=0, a
+    separate process) and as the oracle; weighted fields fall back."""
+    import json
+    import subprocess
+    import sys
+    code = r'''
+import json, sys
+import numpy as np
+sys.path.insert(0, ".")
+from paper_2305_14641_b200 import native as N
+from tests import helpers as H
+out = {}
+for name, g in [("sbm", None), ("rand", H.random_graph(3001, 14, 21, unit=True)),
+                ("weighted", H.random_graph(2001, 9, 22, unit=False))]:
+    if g is None:
+        off, nbr = H.sbm_csr()
+        csr = N.Csr(off, nbr, None, 10.0)
+    else:
+        csr = g.csr(N)
+    res, _, succ = N.cluster_sweep(csr, np.exp(np.linspace(0.0, np.log(30.0), 32)), want_succ=True)
+    out[name] = [int(np.frombuffer(succ.tobytes(), np.uint8).astype(np.int64).sum()), N.last_launch_count(),
+                 [r.num_clusters for r in res], succ.tolist()[::97]]
+print(json.dumps(out))
+'''
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = {}
+    for flag in ("1", "0"):
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                           env=dict(os.environ, GQC_CLASS_ORDER=flag))
+        assert r.returncode == 0, r.stderr[-2000:]
+        runs[flag] = json.loads(r.stdout.strip().splitlines()[-1])
+    for name in ("sbm", "rand", "weighted"):
+        on, off = runs["1"][name], runs["0"][name]
+        assert on[0] == off[0] and on[2] == off[2] and on[3] == off[3], name
+        assert on[1] == off[1] + 10, name  # the class-order launches ran
+    # and the plain path equals the oracle (sampled sigma)
+    g = H.random_graph(3001, 14, 21, unit=True)
+    sig = np.exp(np.linspace(0.0, np.log(30.0), 32))
+    res, v, succ = N.cluster_sweep(g.csr(N), sig, want_v=True, want_succ=True)
+    for q in (0, 9, 31):
+        assert np.array_equal(succ[q], O.build_successors(g.offsets, g.nbr, v[q]))
