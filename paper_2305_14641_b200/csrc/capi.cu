@@ -377,8 +377,11 @@ gqc_csr upload_csr(DeviceCtx& C, const gqc_csr* g, cudaStream_t st, const double
 
 
 // Degree-class order of a field for the GGD argmin fast path (kernels.cu,
-// launch_class_order). Verified per sigma on the field, so it is exact for
-// any input; GQC_CLASS_ORDER=0 disables it (A/B measurements).
+// launch_class_order + successors_class_kernel). Verified per sigma on the
+// field, so exact for any input, but OFF by default (GQC_CLASS_ORDER=1 turns
+// it on): its sort + per-class min/max pass costs about what it saves.
+// Measured (1 B200, 32 sigmas, GGD ms plain -> class order): LFR 1M
+// 1.31 -> 1.19, SBM 100k 0.117 -> 0.216, R-MAT scale 22 6.49 -> 6.68.
 struct ClassOrderScope {
     ClassOrder co;
     void* mem = nullptr;
@@ -395,14 +398,18 @@ struct ClassOrderScope {
 bool class_order_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("GQC_CLASS_ORDER");
-        return !(e && *e == '0');
+        return e && *e == '1';
     }();
     return on;
 }
 
-void make_class_order(DeviceCtx& C, int n, const std::int64_t* off, long long nnz, const double* v, int ld, int S,
-                      cudaStream_t st, ClassOrderScope& out) {
-    if (!class_order_enabled()) return;
+void make_class_order(DeviceCtx& C, const gqc_csr& g, const double* v, int ld, int S, cudaStream_t st,
+                      ClassOrderScope& out) {
+    // weighted graphs and k-hop fields are not degree-determined: plain argmin
+    if (!class_order_enabled() || g.w || g_opt.hop_cap > 1) return;
+    const int n = g.n;
+    const std::int64_t* off = g.offsets;
+    const long long nnz = g.nnz;
     out.st = st;
     cuda_check(launch_class_order(n, off, nnz, v, ld, S, C.pool, st, &out.co, &out.mem), "class order");
 }
@@ -692,7 +699,7 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
                        "copy counts");
         };
         ClassOrderScope order;
-        make_class_order(C, n, d.offsets, nnz, v_nm, n_sigma, n_sigma, st, order);
+        make_class_order(C, d, v_nm, n_sigma, n_sigma, st, order);
         for (std::size_t q = 0; q + 1 < cuts.size(); ++q) {
             const int s0 = cuts[q], Sc = cuts[q + 1] - cuts[q];
             const std::size_t o = static_cast<std::size_t>(s0) * n;
@@ -782,7 +789,7 @@ gqc_status gqc_dev_ggd(const gqc_csr* g, const double* v, int32_t n_sigma, int32
         DeviceCtx& C = ctx(st, g->offsets);
         int* s = succ ? succ : center;  // the chase runs in place on center
         ClassOrderScope order;
-        make_class_order(C, g->n, g->offsets, g->nnz, v, n_sigma, n_sigma, st, order);
+        make_class_order(C, *g, v, n_sigma, n_sigma, st, order);
         cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, 0, g->n, s, 1, g->n, g->nnz, C.pool,
                                      st, order.get()),
                    "successor kernel");
@@ -802,7 +809,7 @@ gqc_status gqc_dev_successors(const gqc_csr* g, const double* v, int32_t n_sigma
         auto st = static_cast<cudaStream_t>(stream);
         DeviceCtx& C = ctx(st, g->offsets);
         ClassOrderScope order;
-        make_class_order(C, g->n, g->offsets, g->nnz, v, n_sigma, n_sigma, st, order);
+        make_class_order(C, *g, v, n_sigma, n_sigma, st, order);
         cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, row_begin, row_end, succ_rows,
                                      n_sigma, 1, g->nnz, C.pool, st, order.get()),
                    "successor kernel");

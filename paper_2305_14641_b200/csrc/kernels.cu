@@ -17,7 +17,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
+#include <string>
+#include <vector>
 #include <utility>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -608,7 +612,7 @@ __device__ __forceinline__ bool lex_less(double va, int ia, double vb, int ib) {
 __global__ void __launch_bounds__(kBlock) successors_kernel(const long long* __restrict__ off,
                                                             const int* __restrict__ nbr,
                                                             const double* __restrict__ v, int ld, int s0, int Sc,
-                                                            int row_begin, int rows, SuccOut O, ClassOrder co) {
+                                                            int row_begin, int rows, SuccOut O) {
     // rows * Sc < 2^31 (launch_successors checks): 32-bit index math
     const unsigned tid = blockIdx.x * static_cast<unsigned>(kBlock) + threadIdx.x;
     const unsigned r = tid / static_cast<unsigned>(Sc);
@@ -623,35 +627,6 @@ __global__ void __launch_bounds__(kBlock) successors_kernel(const long long* __r
     const long long kend = off[i + 1];
     if (kend - k > kHeavyDegree) return;  // heavy rows: successors_heavy_kernel
     int best = i;
-    const int dir = co.dir ? co.dir[s] : 0;
-    if (dir != 0) {
-        // Degree-class fast path (dir verified for this sigma by
-        // launch_class_order): a node of a better class beats every node of a
-        // worse one, so the lexicographic (v, id) minimum lies in the best
-        // class present in the closed neighbourhood; only that class's
-        // potentials are gathered (the class ids are a 4 B, L2-resident gather).
-        const int ci = __ldg(co.cls + i);
-        int bc = ci;
-        for (long long kk = k; kk < kend; ++kk) {
-            const int c = __ldg(co.cls + __ldg(nbr + kk));
-            bc = dir > 0 ? min(bc, c) : max(bc, c);
-        }
-        if (bc != ci) {
-            best = 0x7fffffff;
-            vb = __longlong_as_double(0x7ff0000000000000ll);
-        }
-        for (; k < kend; ++k) {
-            const int j = __ldg(nbr + k);
-            if (__ldg(co.cls + j) != bc) continue;
-            const double vj = __ldg(v + static_cast<long long>(j) * ld + s);
-            if (lex_less(vj, j, vb, best)) {
-                best = j;
-                vb = vj;
-            }
-        }
-        O.out[static_cast<long long>(r) * O.out_row + q * O.out_col] = best;
-        return;
-    }
     // kSuccUnroll independent gathers in flight, compared in ascending k
     for (; k + kSuccUnroll <= kend; k += kSuccUnroll) {
         int j[kSuccUnroll];
@@ -676,6 +651,82 @@ __global__ void __launch_bounds__(kBlock) successors_kernel(const long long* __r
         }
     }
     O.out[static_cast<long long>(r) * O.out_row + q * O.out_col] = best;
+}
+
+// Degree-class fast path of K3 (ClassOrder verified by launch_class_order):
+// a node of a better degree class beats every node of a worse one, so the
+// lexicographic (v, id) minimum of a closed neighbourhood lies in its best
+// class. Warp per light row: lanes take neighbour slots for the class phase
+// (ids and class ids for up to kHeavyDegree neighbours in one round of
+// loads, warp min / max), then lanes are sigmas and only the best-class
+// candidates' potentials are gathered (one 256 B line each). Per row that is
+// ~4 dependent memory levels instead of one gather level per neighbour.
+// Sigmas without a verified order (dir 0) scan every neighbour.
+__global__ void __launch_bounds__(kBlock) successors_class_kernel(const long long* __restrict__ off,
+                                                                  const int* __restrict__ nbr,
+                                                                  const double* __restrict__ v, int ld, int s0,
+                                                                  int Sc, int row_begin, int rows, SuccOut O,
+                                                                  ClassOrder co) {
+    constexpr unsigned kFull = 0xffffffffu;
+    constexpr int kChunks = kHeavyDegree / 32;
+    const int lane = threadIdx.x & 31;
+    const int r = static_cast<int>((blockIdx.x * static_cast<unsigned>(kBlock) + threadIdx.x) >> 5);
+    if (r >= rows) return;
+    const int i = row_begin + r;
+    const long long kb = off[i], ke = off[i + 1];
+    if (ke - kb > kHeavyDegree) return;  // heavy rows: successors_heavy_kernel
+    const int s = s0 + min(lane, Sc - 1);
+    const int dir = __ldg(co.dir + s);
+    const int ci = __ldg(co.cls + i);
+    double vb = __ldg(v + static_cast<long long>(i) * ld + s);
+    int jr[kChunks], cr[kChunks];
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+        const long long k = kb + 32 * q + lane;
+        jr[q] = k < ke ? __ldg(nbr + k) : -1;
+    }
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) cr[q] = jr[q] >= 0 ? __ldg(co.cls + jr[q]) : ci;
+    int cmin = ci, cmax = ci;
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+        cmin = min(cmin, cr[q]);
+        cmax = max(cmax, cr[q]);
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        cmin = min(cmin, __shfl_xor_sync(kFull, cmin, d));
+        cmax = max(cmax, __shfl_xor_sync(kFull, cmax, d));
+    }
+    const int bc = dir > 0 ? cmin : cmax;
+    int best = i;
+    if (dir != 0 && ci != bc) {
+        best = 0x7fffffff;
+        vb = __longlong_as_double(0x7ff0000000000000ll);
+    }
+#pragma unroll
+    for (int q = 0; q < kChunks; ++q) {
+        if (kb + 32 * q >= ke) break;  // warp-uniform
+        const bool valid = jr[q] >= 0;
+        const unsigned m_lo = __ballot_sync(kFull, valid && cr[q] == cmin);
+        const unsigned m_hi = __ballot_sync(kFull, valid && cr[q] == cmax);
+        const unsigned m_all = __ballot_sync(kFull, valid);
+        const unsigned mine = dir > 0 ? m_lo : (dir < 0 ? m_hi : m_all);
+        unsigned u = __reduce_or_sync(kFull, mine);
+        while (u) {
+            const int t = __ffs(u) - 1;
+            u &= u - 1;
+            const int j = __shfl_sync(kFull, jr[q], t);
+            if ((mine >> t) & 1u) {
+                const double vj = __ldg(v + static_cast<long long>(j) * ld + s);
+                if (lex_less(vj, j, vb, best)) {
+                    best = j;
+                    vb = vj;
+                }
+            }
+        }
+    }
+    if (lane < Sc) O.out[static_cast<long long>(r) * O.out_row + lane * O.out_col] = best;
 }
 
 // Heavy rows (degree > kHeavyDegree, e.g. R-MAT hubs with ~10^5 neighbours)
@@ -1229,6 +1280,16 @@ int launch_class_order(int n, const std::int64_t* offsets, long long nnz, const 
     count_launch(10);
     out->cls = cls;
     out->dir = dir;
+    if (const char* t = std::getenv("GQC_TRACE"); t && *t && *t != '0') {  // which sigmas verified
+        std::vector<signed char> h(S);
+        int C = 0;
+        cudaMemcpyAsync(h.data(), dir, S, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(&C, cidx + n - 1, sizeof(int), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        std::string line = "[gqc trace] class order: " + std::to_string(C) + " degree classes, dir =";
+        for (int q = 0; q < S; ++q) line += " " + std::to_string(static_cast<int>(h[q]));
+        std::fprintf(stderr, "%s\n", line.c_str());
+    }
     return cudaGetLastError();
 }
 
@@ -1275,8 +1336,11 @@ int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nb
         const SuccOut O{out + c0 * out_col, out_row, out_col};
         const long long threads = static_cast<long long>(rows) * Sc;
         if (threads >= (1ll << 31) - kBlock) return cudaErrorInvalidValue;  // 32-bit thread ids
-        successors_kernel<<<grid_for(threads), kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, rows, O,
-                                                                 co ? *co : ClassOrder{});
+        if (co && co->dir)
+            successors_class_kernel<<<grid_for(static_cast<long long>(rows) * 32), kBlock, 0, st>>>(
+                off, nbr, v, ld, s0 + c0, Sc, row_begin, rows, O, *co);
+        else
+            successors_kernel<<<grid_for(threads), kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, rows, O);
         successors_heavy_kernel<<<num_sms * 8, kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, items, counts,
                                                                  part_v, part_i, O);
         successors_combine_kernel<<<num_sms * 2, kBlock, 0, st>>>(multi, counts, part_v, part_i, Sc, row_begin, O);
