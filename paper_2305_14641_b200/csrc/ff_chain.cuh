@@ -14,6 +14,10 @@
 #define GQC_HD
 #endif
 
+#ifndef GQC_STEP_FINISH
+#define GQC_STEP_FINISH 1
+#endif
+
 namespace gqc {
 namespace ffc {
 
@@ -249,6 +253,17 @@ GQC_HD inline void ff_step(Chain& ch, const double c, int& L) {
         ch.top = gqc_add(top, top);  // landed in [top, 2 top): see ff_pass
         ch.inc = gqc_sub(gqc_add(top, c), top);
         ch.flags = kJump | (exp_field(top) == ch.f_tie ? kTie : 0);
+#if GQC_STEP_FINISH
+        // finish the run in the new binade when it fits (a single-crossing
+        // run then costs one trip of ff_walk2's loop instead of two)
+        if (L > 0 && settled(ch)) {
+            const double t2 = gqc_fma(static_cast<double>(L), ch.inc, ch.s);
+            if (t2 < ch.top) {
+                ch.s = t2;
+                L = 0;
+            }
+        }
+#endif
     } else {
         ch.s = gqc_add(ch.s, c);
         --L;
