@@ -14,8 +14,11 @@
 #define GQC_HD
 #endif
 
+// GQC_STEP_FINISH=1: ff_step also finishes a run inside the new binade after
+// a settled crossing. Measured: LFR potentials 4.49 -> 4.44 ms but R-MAT
+// 10.51 -> 10.90 ms (register pressure in the batched kernel), so off.
 #ifndef GQC_STEP_FINISH
-#define GQC_STEP_FINISH 1
+#define GQC_STEP_FINISH 0
 #endif
 
 namespace gqc {

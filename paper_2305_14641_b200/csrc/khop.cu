@@ -31,6 +31,8 @@
 #include <climits>
 #include <vector>
 
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
@@ -51,6 +53,9 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr std::size_t kSmemBitsetBytes = 200 * 1024;
 // Events held in device memory at once (keys + sorted keys): 2 x 4 B each.
 constexpr long long kEventBudget = 1ll << 30;
+// On-chip sorted emission (hop cap 2): rows with at most kSortCap candidates.
+// Two sizes: 128 x 4 (<= 512 candidates) and 256 x 8 (<= 2048).
+constexpr long long kSortCap0 = 128 * 4, kSortCap1 = 256 * 8;
 
 struct KhopExpand {
     int n;
@@ -66,6 +71,8 @@ struct KhopExpand {
     unsigned* scratch;         // count pass: [gridDim.x][n] per-block level lists
     unsigned* gbits;           // [gridDim.x][words] global bitsets, or nullptr (shared)
     int words;
+    const int* list;           // hop cap 2 emission: the pass's rows (pass-relative), or nullptr = all
+    const int* list_len;
 };
 
 template <bool kFill>
@@ -133,6 +140,115 @@ __global__ void __launch_bounds__(kExpandThreads) khop_expand_kernel(const KhopE
     }
 }
 
+// Hop cap 2, rows whose candidate bound (sum of the neighbours' degrees)
+// fits kThreads * kItems: block per row with everything on chip and many
+// rows in flight per SM (the bitset kernel above holds one N-bit row per SM):
+// the neighbours' rows are gathered into shared memory (warp per neighbour,
+// coalesced), block radix sorted (cub::BlockRadixSort, bits of N only), and
+// the sorted candidates are kept when new, not the row itself and not in its
+// CSR row (binary search); a block scan places them, already in column order.
+template <int kThreads, int kItems>
+__global__ void __launch_bounds__(kThreads) khop2_sort_kernel(const KhopExpand E, int end_bit) {
+    constexpr int kCap = kThreads * kItems;
+    constexpr int kWarps = kThreads / 32;
+    using Sort = cub::BlockRadixSort<unsigned, kThreads, kItems>;
+    using Scan = cub::BlockScan<int, kThreads>;
+    __shared__ union {
+        typename Sort::TempStorage sort;
+        typename Scan::TempStorage scan;
+    } tmp;
+    __shared__ unsigned keys[kCap];
+    __shared__ int row_nb[kCap];
+    __shared__ int s_row, s_cnt, s_tot;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nrows = *E.list_len;
+    for (;;) {
+        if (tid == 0) {
+            s_row = atomicAdd(E.counter, 1);
+            s_cnt = 0;
+        }
+        __syncthreads();
+        const int idx = s_row;
+        if (idx >= nrows) break;
+        const int r = E.list[idx];
+        const int i = E.row_begin + r;
+        const long long kb = E.off[i];
+        const int deg = static_cast<int>(E.off[i + 1] - kb);  // <= bound <= kCap
+        for (int k = tid; k < deg; k += kThreads) row_nb[k] = E.nbr[kb + k];
+        __syncthreads();
+        for (int f = warp; f < deg; f += kWarps) {  // warp per neighbour
+            const int u = row_nb[f];
+            const long long ub = E.off[u], ue = E.off[u + 1];
+            int base = 0;
+            if (lane == 0) base = atomicAdd(&s_cnt, static_cast<int>(ue - ub));
+            base = __shfl_sync(kFull, base, 0);
+            for (long long k = ub + lane; k < ue; k += 32) keys[base + (k - ub)] = static_cast<unsigned>(E.nbr[k]);
+        }
+        __syncthreads();
+        const int cnt = s_cnt;
+        unsigned item[kItems];
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) {
+            const int p = tid * kItems + q;
+            item[q] = p < cnt ? keys[p] : 0xffffffffu;  // padding sorts last (low end_bit bits all ones)
+        }
+        Sort(tmp.sort).Sort(item, 0, end_bit);
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) keys[tid * kItems + q] = item[q];
+        __syncthreads();
+        bool keep[kItems];
+        int nkeep = 0;
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) {
+            const int p = tid * kItems + q;
+            const int c = static_cast<int>(item[q]);
+            bool k = p < cnt && c != i && (p == 0 || keys[p - 1] != item[q]);
+            if (k) {  // not a hop-1 neighbour (the CSR row is ascending)
+                int lo = 0, hi = deg;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (row_nb[mid] < c) lo = mid + 1;
+                    else hi = mid;
+                }
+                k = !(lo < deg && row_nb[lo] == c);
+            }
+            keep[q] = k;
+            nkeep += k;
+        }
+        int pos = 0, total = 0;
+        Scan(tmp.scan).ExclusiveSum(nkeep, pos, total);
+        unsigned* dst = E.ev + (E.ev_off[r] - E.ev_base);
+#pragma unroll
+        for (int q = 0; q < kItems; ++q)
+            if (keep[q]) dst[pos++] = (item[q] << 3) | 2u;
+        if (tid == 0) E.count[r] = total;
+        __syncthreads();
+    }
+}
+
+// Rows of a pass split by their candidate bound: <= cap0 and <= cap1 to the
+// two sort-kernel sizes, the rest to the bitset kernel (warp-aggregated
+// appends into lists[0..2], lengths in lens[0..2]).
+__global__ void khop_split_kernel(const long long* __restrict__ ev_off, int rows, long long cap0, long long cap1,
+                                  int* __restrict__ list0, int* __restrict__ list1, int* __restrict__ list2,
+                                  int* __restrict__ lens) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool valid = r < rows;
+    const long long b = valid ? ev_off[r + 1] - ev_off[r] : 0;
+    const int cls = !valid ? -1 : (b <= cap0 ? 0 : (b <= cap1 ? 1 : 2));
+    int* lists[3] = {list0, list1, list2};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const unsigned m = __ballot_sync(kFull, cls == c);
+        int base = 0;
+        if (lane == 0 && m) base = atomicAdd(&lens[c], __popc(m));
+        base = __shfl_sync(kFull, base, 0);
+        if (cls == c) lists[c][base + __popc(m & ((1u << lane) - 1u))] = r;
+    }
+}
+
 // Row segments of a batch relative to its first row: [seg_b, seg_e) = the
 // events the fill pass wrote (offsets may be upper bounds, hop cap 2).
 // Hop cap 2 with the bitset on chip: the events are emitted already sorted.
@@ -157,11 +273,13 @@ __global__ void __launch_bounds__(kThreads) khop2_emit_kernel(const KhopExpand E
     const int spt = (swords + kThreads - 1) / kThreads;  // summary words per thread
     for (int w = tid; w < E.words + swords; w += kThreads) bits[w] = 0u;
     __syncthreads();
+    const int nrows = E.list ? *E.list_len : E.rows;
     for (;;) {
         if (tid == 0) s_row = atomicAdd(E.counter, 1);
         __syncthreads();
-        const int r = s_row;
-        if (r >= E.rows) break;
+        const int idx = s_row;
+        if (idx >= nrows) break;
+        const int r = E.list ? E.list[idx] : idx;
         const int i = E.row_begin + r;
         const long long kb = E.off[i], ke = E.off[i + 1];
         for (long long f = warp; f < ke - kb; f += kWarps) {  // warp per neighbour
@@ -581,6 +699,8 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
         }
         emit_grid = num_sms() * std::max(per, 1);
     }
+    int sort_end_bit = 1;  // keys < n: the padding 0xffffffff must sort after every key
+    while (sort_end_bit < 32 && (1ll << sort_end_bit) <= n) ++sort_end_bit;
     int walk_grid_cap = num_sms() * kWalkBlocksPerSM;
     for (std::size_t b = 0; b + 1 < cuts.size(); ++b) {
         const int r0 = cuts[b], r1 = cuts[b + 1], nr = r1 - r0;
@@ -596,8 +716,8 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
         const std::size_t b_seg = 2 * bytes_of((nr + 1) * sizeof(int));
         const std::size_t b_key = bytes_of(nr * sizeof(int));
         void* bm = nullptr;
-        if ((e = cudaMallocFromPoolAsync(&bm, 2 * b_ev + b_seg + 4 * b_key + bytes_of(sort_bytes) +
-                                                  bytes_of(key_bytes) + 256,
+        if ((e = cudaMallocFromPoolAsync(&bm, 2 * b_ev + b_seg + 7 * b_key + bytes_of(sort_bytes) +
+                                                  bytes_of(key_bytes) + 512,
                                          pool, st)) != cudaSuccess)
             return e;
         char* q = static_cast<char*>(bm);
@@ -612,6 +732,10 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
         int* wcounter = reinterpret_cast<int*>(q + 2 * b_ev + b_seg + 4 * b_key);
         void* sort_tmp = q + 2 * b_ev + b_seg + 4 * b_key + 256;
         void* key_tmp = static_cast<char*>(sort_tmp) + bytes_of(sort_bytes);
+        int* rows0 = reinterpret_cast<int*>(static_cast<char*>(key_tmp) + bytes_of(key_bytes));
+        int* rows1 = rows0 + b_key / sizeof(int);
+        int* rows2 = rows1 + b_key / sizeof(int);
+        int* lens = rows2 + b_key / sizeof(int);  // list lengths
 
         // fill pass over the batch's rows
         KhopExpand F = E;
@@ -625,14 +749,34 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
         const unsigned* ev_walk = ev_sorted;
         if (emit) {
             F.ev = ev_sorted;  // written in column order
-            if (big_emit)
-                khop2_emit_kernel<1024><<<std::max(1, std::min(emit_grid, nr)), 1024, edyn, st>>>(F);
-            else
+            if (big_emit) {
+                // the bitset holds one row per SM: rows whose candidates fit on
+                // chip go to the sort kernel (many rows in flight), the rest
+                // to the bitset kernel
+                cudaMemsetAsync(lens, 0, 4 * sizeof(int), st);
+                khop_split_kernel<<<(nr + 255) / 256, 256, 0, st>>>(ev_off + r0, nr, kSortCap0, kSortCap1, rows0,
+                                                                     rows1, rows2, lens);
+                KhopExpand F0 = F, F1 = F, F2 = F;
+                F0.list = rows0;
+                F0.list_len = lens;
+                F1.list = rows1;
+                F1.list_len = lens + 1;
+                F1.counter = counter + 1;
+                F2.list = rows2;
+                F2.list_len = lens + 2;
+                F2.counter = counter + 2;
+                khop2_sort_kernel<128, 4><<<num_sms() * 8, 128, 0, st>>>(F0, sort_end_bit);
+                khop2_sort_kernel<256, 8><<<num_sms() * 4, 256, 0, st>>>(F1, sort_end_bit);
+                khop2_emit_kernel<1024><<<std::max(1, std::min(emit_grid, nr)), 1024, edyn, st>>>(F2);
+                count_launch(4);
+            } else {
                 khop2_emit_kernel<256><<<std::max(1, std::min(emit_grid, nr)), 256, edyn, st>>>(F);
+                count_launch();
+            }
         } else {
             khop_expand_kernel<true><<<std::max(1, std::min(grid, nr)), kExpandThreads, dyn, st>>>(F);
+            count_launch();
         }
-        count_launch();
         khop_segments_kernel<<<(nr + 255) / 256, 256, 0, st>>>(ev_off + r0, count + r0, nr, seg_b, seg_e);
         count_launch();
         if (items > 0 && !emit) {
