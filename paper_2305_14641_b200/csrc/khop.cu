@@ -64,7 +64,7 @@ struct KhopExpand {
     int row_begin, rows;  // this pass covers rows [row_begin, row_begin + rows)
     int K;
     int* counter;              // row queue
-    long long* count;          // hop >= 2 nodes of each row (both passes write it)
+    long long* count;          // events of each row, hops 1..K (both passes write it)
     const long long* ev_off;   // fill pass: event offset of each row (absolute)
     long long ev_base;         // fill pass: ev_off value of the pass's first row
     unsigned* ev;              // fill pass: events (col << 3 | hop), relative to ev_base
@@ -84,25 +84,28 @@ __global__ void __launch_bounds__(kExpandThreads) khop_expand_kernel(const KhopE
     for (int w = tid; w < E.words; w += blockDim.x) bits[w] = 0u;
     __syncthreads();
     for (;;) {
-        if (tid == 0) {
-            s_row = atomicAdd(E.counter, 1);
-            s_pos = 0;
-        }
+        if (tid == 0) s_row = atomicAdd(E.counter, 1);
         __syncthreads();
         const int r = s_row;
         if (r >= E.rows) break;
         const int i = E.row_begin + r;
         const long long kb = E.off[i], ke = E.off[i + 1];
+        const int deg = static_cast<int>(ke - kb);
         unsigned* dst = kFill ? E.ev + (E.ev_off[r] - E.ev_base)
                               : E.scratch + static_cast<std::size_t>(blockIdx.x) * E.n;
-        // hop 0 and 1: the row itself and its CSR neighbours
-        if (tid == 0) atomicOr(&bits[i >> 5], 1u << (i & 31));
+        // hop 0 and 1: the row itself and its CSR neighbours (the hop-1
+        // events open the row's list; deeper levels are appended after them)
+        if (tid == 0) {
+            atomicOr(&bits[i >> 5], 1u << (i & 31));
+            s_pos = deg;
+        }
         for (long long k = kb + tid; k < ke; k += blockDim.x) {
             const int c = E.nbr[k];
             atomicOr(&bits[c >> 5], 1u << (c & 31));
+            dst[k - kb] = (static_cast<unsigned>(c) << 3) | 1u;
         }
         __syncthreads();
-        int lvl_b = 0, lvl_e = 0;
+        int lvl_b = deg, lvl_e = deg;
         for (int h = 2; h <= E.K; ++h) {
             const long long nf = (h == 2) ? (ke - kb) : (lvl_e - lvl_b);
             // warp per frontier vertex: its row in coalesced 32-wide chunks
@@ -140,13 +143,15 @@ __global__ void __launch_bounds__(kExpandThreads) khop_expand_kernel(const KhopE
     }
 }
 
-// Hop cap 2, rows whose candidate bound (sum of the neighbours' degrees)
-// fits kThreads * kItems: block per row with everything on chip and many
-// rows in flight per SM (the bitset kernel above holds one N-bit row per SM):
-// the neighbours' rows are gathered into shared memory (warp per neighbour,
-// coalesced), block radix sorted (cub::BlockRadixSort, bits of N only), and
-// the sorted candidates are kept when new, not the row itself and not in its
-// CSR row (binary search); a block scan places them, already in column order.
+// Hop cap 2, rows whose candidates (the CSR row plus every neighbour's row)
+// fit kThreads * kItems: block per row with everything on chip and many rows
+// in flight per SM (the bitset kernel below holds one N-bit row per SM). The
+// candidates are gathered into shared memory as (col << 1 | 0) for the row's
+// own neighbours and (col << 1 | 1) for its neighbours' neighbours (warp per
+// neighbour, coalesced), block radix sorted (cub::BlockRadixSort, bits of N
+// plus one), and the first entry of every column other than the row itself
+// is kept: hop 1 when the row lists it, else hop 2. A block scan places the
+// events, already in column order.
 template <int kThreads, int kItems>
 __global__ void __launch_bounds__(kThreads) khop2_sort_kernel(const KhopExpand E, int end_bit) {
     constexpr int kCap = kThreads * kItems;
@@ -158,31 +163,29 @@ __global__ void __launch_bounds__(kThreads) khop2_sort_kernel(const KhopExpand E
         typename Scan::TempStorage scan;
     } tmp;
     __shared__ unsigned keys[kCap];
-    __shared__ int row_nb[kCap];
-    __shared__ int s_row, s_cnt, s_tot;
+    __shared__ int s_row, s_cnt;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nrows = *E.list_len;
     for (;;) {
-        if (tid == 0) {
-            s_row = atomicAdd(E.counter, 1);
-            s_cnt = 0;
-        }
+        if (tid == 0) s_row = atomicAdd(E.counter, 1);
         __syncthreads();
         const int idx = s_row;
         if (idx >= nrows) break;
         const int r = E.list[idx];
         const int i = E.row_begin + r;
         const long long kb = E.off[i];
-        const int deg = static_cast<int>(E.off[i + 1] - kb);  // <= bound <= kCap
-        for (int k = tid; k < deg; k += kThreads) row_nb[k] = E.nbr[kb + k];
+        const int deg = static_cast<int>(E.off[i + 1] - kb);  // deg + sum of their degrees <= kCap
+        if (tid == 0) s_cnt = deg;
+        for (int k = tid; k < deg; k += kThreads) keys[k] = static_cast<unsigned>(E.nbr[kb + k]) << 1;
         __syncthreads();
         for (int f = warp; f < deg; f += kWarps) {  // warp per neighbour
-            const int u = row_nb[f];
+            const int u = static_cast<int>(keys[f] >> 1);
             const long long ub = E.off[u], ue = E.off[u + 1];
             int base = 0;
             if (lane == 0) base = atomicAdd(&s_cnt, static_cast<int>(ue - ub));
             base = __shfl_sync(kFull, base, 0);
-            for (long long k = ub + lane; k < ue; k += 32) keys[base + (k - ub)] = static_cast<unsigned>(E.nbr[k]);
+            for (long long k = ub + lane; k < ue; k += 32)
+                keys[base + (k - ub)] = (static_cast<unsigned>(E.nbr[k]) << 1) | 1u;
         }
         __syncthreads();
         const int cnt = s_cnt;
@@ -202,26 +205,16 @@ __global__ void __launch_bounds__(kThreads) khop2_sort_kernel(const KhopExpand E
 #pragma unroll
         for (int q = 0; q < kItems; ++q) {
             const int p = tid * kItems + q;
-            const int c = static_cast<int>(item[q]);
-            bool k = p < cnt && c != i && (p == 0 || keys[p - 1] != item[q]);
-            if (k) {  // not a hop-1 neighbour (the CSR row is ascending)
-                int lo = 0, hi = deg;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (row_nb[mid] < c) lo = mid + 1;
-                    else hi = mid;
-                }
-                k = !(lo < deg && row_nb[lo] == c);
-            }
-            keep[q] = k;
-            nkeep += k;
+            const unsigned c = item[q] >> 1;
+            keep[q] = p < cnt && c != static_cast<unsigned>(i) && (p == 0 || (keys[p - 1] >> 1) != c);
+            nkeep += keep[q];
         }
         int pos = 0, total = 0;
         Scan(tmp.scan).ExclusiveSum(nkeep, pos, total);
         unsigned* dst = E.ev + (E.ev_off[r] - E.ev_base);
 #pragma unroll
         for (int q = 0; q < kItems; ++q)
-            if (keep[q]) dst[pos++] = (item[q] << 3) | 2u;
+            if (keep[q]) dst[pos++] = ((item[q] >> 1) << 3) | ((item[q] & 1u) ? 2u : 1u);
         if (tid == 0) E.count[r] = total;
         __syncthreads();
     }
@@ -249,18 +242,17 @@ __global__ void khop_split_kernel(const long long* __restrict__ ev_off, int rows
     }
 }
 
-// Row segments of a batch relative to its first row: [seg_b, seg_e) = the
-// events the fill pass wrote (offsets may be upper bounds, hop cap 2).
 // Hop cap 2 with the bitset on chip: the events are emitted already sorted.
-// Block per source row (rows from a queue): every neighbour's row is OR-ed
-// into the shared-memory bitset (warp per neighbour, coalesced 32-wide
-// chunks; a word that turns non-zero also sets its bit in a summary bitset,
-// one bit per word), the row itself and its neighbours are cleared again,
+// Block per source row (rows from a queue): the row's own neighbours and
+// every neighbour's row are OR-ed into the shared-memory bitset (warp per
+// neighbour, coalesced 32-wide chunks; a word that turns non-zero also sets
+// its bit in a summary bitset, one bit per word), the row itself is cleared,
 // and the summary is walked in column order: thread t owns a contiguous run
 // of summary words, counts the columns under them, a block scan gives each
-// thread its output position, and it writes its columns ascending and zeroes
-// what it visited. Work per row is proportional to its events, not to N; no
-// per-row sort and no second BFS.
+// thread its output position, and it writes its columns ascending (hop 1 when
+// the CSR row lists it, by binary search, else hop 2) and zeroes what it
+// visited. Work per row is proportional to its events, not to N; no per-row
+// sort and no second BFS.
 template <int kThreads>
 __global__ void __launch_bounds__(kThreads) khop2_emit_kernel(const KhopExpand E) {
     extern __shared__ unsigned bits[];  // [words] bitset, then [swords] summary
@@ -292,10 +284,12 @@ __global__ void __launch_bounds__(kThreads) khop2_emit_kernel(const KhopExpand E
             }
         }
         __syncthreads();
-        for (long long k = kb + tid; k < ke; k += kThreads) {  // hop 1 is not a hop-2 event
+        for (long long k = kb + tid; k < ke; k += kThreads) {  // hop 1 (not every neighbour is 2 hops away)
             const int c = E.nbr[k];
-            atomicAnd(&bits[c >> 5], ~(1u << (c & 31)));
+            const int x = c >> 5;
+            if (atomicOr(&bits[x], 1u << (c & 31)) == 0u) atomicOr(&summ[x >> 5], 1u << (x & 31));
         }
+        __syncthreads();
         if (tid == 0) atomicAnd(&bits[i >> 5], ~(1u << (i & 31)));
         __syncthreads();
         // count the columns under this thread's summary words
@@ -340,7 +334,14 @@ __global__ void __launch_bounds__(kThreads) khop2_emit_kernel(const KhopExpand E
                 bits[x] = 0u;
                 const unsigned col0 = static_cast<unsigned>(x) << 5;
                 while (v) {
-                    dst[pos++] = ((col0 + (__ffs(v) - 1)) << 3) | 2u;
+                    const int c = static_cast<int>(col0) + (__ffs(v) - 1);
+                    long long lo = kb, hi = ke;  // hop 1 iff the CSR row lists c
+                    while (lo < hi) {
+                        const long long mid = (lo + hi) >> 1;
+                        if (__ldg(E.nbr + mid) < c) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    dst[pos++] = (static_cast<unsigned>(c) << 3) | ((lo < ke && __ldg(E.nbr + lo) == c) ? 1u : 2u);
                     v &= v - 1;
                 }
             }
@@ -350,6 +351,8 @@ __global__ void __launch_bounds__(kThreads) khop2_emit_kernel(const KhopExpand E
     }
 }
 
+// Row segments of a batch relative to its first row: [seg_b, seg_e) = the
+// events the fill pass wrote (offsets may be upper bounds, hop cap 2).
 __global__ void khop_segments_kernel(const long long* __restrict__ ev_off, const long long* __restrict__ count,
                                      int rows, int* __restrict__ seg_b, int* __restrict__ seg_e) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -359,8 +362,8 @@ __global__ void khop_segments_kernel(const long long* __restrict__ ev_off, const
     }
 }
 
-// Hop cap 2: an upper bound of each row's hop-2 count without a BFS pass,
-// the sum of its neighbours' degrees (warp per row).
+// Hop cap 2: an upper bound of each row's event count without a BFS pass,
+// its degree plus the sum of its neighbours' degrees (warp per row).
 __global__ void khop_bound_kernel(const long long* __restrict__ off, const int* __restrict__ nbr, int row_begin,
                                   int rows, long long* __restrict__ bound) {
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -372,7 +375,7 @@ __global__ void khop_bound_kernel(const long long* __restrict__ off, const int* 
         acc += off[u + 1] - off[u];
     }
     for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
-    if (lane == 0) bound[w] = acc;
+    if (lane == 0) bound[w] = acc + (off[i + 1] - off[i]);  // + the row's own hop-1 events
 }
 
 __global__ void khop_keys_kernel(const long long* __restrict__ off, const long long* __restrict__ count, int row_begin,
@@ -380,7 +383,7 @@ __global__ void khop_keys_kernel(const long long* __restrict__ off, const long l
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= rows) return;
     const int i = row_begin + k;
-    const long long w = (off[i + 1] - off[i]) + count[k];
+    const long long w = count[k];  // events incl. hop 1
     key[k] = static_cast<int>(min(w, static_cast<long long>(INT_MAX)));
     id[k] = k;
 }
@@ -406,10 +409,11 @@ struct ChunkEvents {
 };
 
 // Walk of rows whose batch-relative index comes from `order` (heaviest
-// first): lane s = sigma s, the merge of hop-1 (CSR) and hop >= 2 (events)
-// columns is warp-uniform. kBatch (hop cap 2): the merged events are taken
-// 32 at a time and walked with walk_events_multi (batched in-binade jumps,
-// ff_chain.cuh); otherwise one event at a time.
+// first): lane s = sigma s; the row's events (hops 1..K in column order, one
+// list) are read 32 at a time with one coalesced load, so the walk is
+// warp-uniform. kBatch (hop cap 2): each chunk is walked with
+// walk_events_multi (batched in-binade jumps, ff_chain.cuh); otherwise one
+// event at a time.
 template <bool kBatch>
 __global__ void __launch_bounds__(kWalkBlock, kWalkBlocksPerSM)
     khop_walk_kernel(const __grid_constant__ PotentialLaunch P, const __grid_constant__ KhopTable T,
@@ -437,7 +441,7 @@ __global__ void __launch_bounds__(kWalkBlock, kWalkBlocksPerSM)
         st[3][h][q] = T.pt[h][q];
     }
     constexpr int kWarps = kWalkBlock / 32;
-    __shared__ int s_a[kBatch ? kWarps : 1][32], s_b[kBatch ? kWarps : 1][32], s_cols[kBatch ? kWarps : 1][32];
+    __shared__ int s_cols[kBatch ? kWarps : 1][32];
     __shared__ unsigned char s_kls[kBatch ? kWarps : 1][32];
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -482,60 +486,26 @@ __global__ void __launch_bounds__(kWalkBlock, kWalkBlocksPerSM)
             den.s = __dadd_rn(den.s, e);
             pos = col + 1;
         };
-        // merge hop 1 (CSR row, ascending) with hop >= 2 (sorted events)
-        long long ka = P.offsets[i];
-        const long long ka_end = P.offsets[i + 1];
+        // the row's events (hops 1..K), ascending columns
         long long kb = seg_b[rb];
         const long long kb_end = seg_e[rb];
         if constexpr (kBatch) {
             const int wslot = threadIdx.x >> 5;
-            int* a_s = s_a[wslot];
-            int* b_s = s_b[wslot];
             int* cols = s_cols[wslot];
             unsigned char* kls = s_kls[wslot];
             const double cn[2] = {st[1][1][s], st[1][2][s]}, cd[2] = {st[0][1][s], st[0][2][s]};
             const int tn[2] = {tie_binade(cn[0]), tie_binade(cn[1])}, td[2] = {tie_binade(cd[0]), tie_binade(cd[1])};
             const int tie_pW = tie_binade(pW), tie_eW = tie_binade(eW);
-            while (ka < ka_end || kb < kb_end) {  // warp-uniform
-                // next 32 events of the merge: ranks within the two 32-windows
-                const int a_l = (ka + lane < ka_end) ? __ldg(P.nbr + ka + lane) : INT_MAX;
-                const int b_l = (kb + lane < kb_end) ? static_cast<int>(__ldg(ev + kb + lane) >> 3) : INT_MAX;
+            for (; kb < kb_end; kb += 32) {  // warp-uniform: 32 events per chunk
+                const int cnt = static_cast<int>(min(32ll, kb_end - kb));
+                const unsigned evl = lane < cnt ? __ldg(ev + kb + lane) : 0xffffffffu;
+                const int my = lane < cnt ? static_cast<int>(evl >> 3) : INT_MAX;
                 __syncwarp();
-                a_s[lane] = a_l;
-                b_s[lane] = b_l;
+                cols[lane] = my;
+                kls[lane] = static_cast<unsigned char>((evl & 7u) - 1u);
                 __syncwarp();
-                int lo = 0, hi = 32;  // #b < a_l
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (b_s[mid] < a_l) lo = mid + 1;
-                    else hi = mid;
-                }
-                const int pa = lane + lo;
-                lo = 0;
-                hi = 32;  // #a < b_l
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (a_s[mid] < b_l) lo = mid + 1;
-                    else hi = mid;
-                }
-                const int pb = lane + lo;
-                const bool va = a_l != INT_MAX && pa < 32, vb = b_l != INT_MAX && pb < 32;
-                if (va) {
-                    cols[pa] = a_l;
-                    kls[pa] = 0;
-                }
-                if (vb) {
-                    cols[pb] = b_l;
-                    kls[pb] = 1;
-                }
-                const unsigned ma = __ballot_sync(kFull, va), mb = __ballot_sync(kFull, vb);
-                ka += __popc(ma);
-                kb += __popc(mb);
-                const int cnt = __popc(ma) + __popc(mb);
-                __syncwarp();
-                const int my = lane < cnt ? cols[lane] : INT_MAX;
-                ChunkEvents ce{cols, kls, __ballot_sync(kFull, lane < cnt && kls[lane] == 0),
-                               __ballot_sync(kFull, lane < cnt && kls[lane] == 1)};
+                ChunkEvents ce{cols, kls, __ballot_sync(kFull, lane < cnt && (evl & 7u) == 1u),
+                               __ballot_sync(kFull, lane < cnt && (evl & 7u) == 2u)};
                 const int jend = (tail && cols[cnt - 1] == n - 1) ? cnt - 1 : cnt;
                 const int before_self = __popc(__ballot_sync(kFull, my < i));
                 int j = 0;
@@ -556,25 +526,12 @@ __global__ void __launch_bounds__(kWalkBlock, kWalkBlocksPerSM)
                 __syncwarp();
             }
         } else {
-            long long base_a = ka, base_b = kb;
-            int buf_a = (ka + lane < ka_end) ? __ldg(P.nbr + ka + lane) : INT_MAX;
-            unsigned buf_b = (kb + lane < kb_end) ? __ldg(ev + kb + lane) : 0xffffffffu;
-            while (ka < ka_end || kb < kb_end) {  // warp-uniform
-                const int ca = __shfl_sync(kFull, buf_a, static_cast<int>(ka - base_a));
-                const unsigned eb = __shfl_sync(kFull, buf_b, static_cast<int>(kb - base_b));
-                const int cb = kb < kb_end ? static_cast<int>(eb >> 3) : INT_MAX;
-                if (ka < ka_end && ca < cb) {
-                    event(ca, 1);
-                    if (++ka - base_a == 32) {
-                        base_a = ka;
-                        buf_a = (ka + lane < ka_end) ? __ldg(P.nbr + ka + lane) : INT_MAX;
-                    }
-                } else {
-                    event(cb, static_cast<int>(eb & 7u));
-                    if (++kb - base_b == 32) {
-                        base_b = kb;
-                        buf_b = (kb + lane < kb_end) ? __ldg(ev + kb + lane) : 0xffffffffu;
-                    }
+            for (; kb < kb_end; kb += 32) {  // one event at a time, 32 loaded per chunk
+                const int cnt = static_cast<int>(min(32ll, kb_end - kb));
+                const unsigned evl = lane < cnt ? __ldg(ev + kb + lane) : 0u;
+                for (int q = 0; q < cnt; ++q) {
+                    const unsigned e = __shfl_sync(kFull, evl, q);
+                    event(static_cast<int>(e >> 3), static_cast<int>(e & 7u));
                 }
             }
         }
@@ -699,8 +656,8 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
         }
         emit_grid = num_sms() * std::max(per, 1);
     }
-    int sort_end_bit = 1;  // keys < n: the padding 0xffffffff must sort after every key
-    while (sort_end_bit < 32 && (1ll << sort_end_bit) <= n) ++sort_end_bit;
+    int sort_end_bit = 1;  // keys (col << 1 | tag) < 2n: the padding 0xffffffff must sort after every key
+    while (sort_end_bit < 32 && (1ll << sort_end_bit) <= 2ll * n) ++sort_end_bit;
     int walk_grid_cap = num_sms() * kWalkBlocksPerSM;
     for (std::size_t b = 0; b + 1 < cuts.size(); ++b) {
         const int r0 = cuts[b], r1 = cuts[b + 1], nr = r1 - r0;
