@@ -258,6 +258,8 @@ __global__ void __launch_bounds__(kThreads) khop2_emit_kernel(const KhopExpand E
     extern __shared__ unsigned bits[];  // [words] bitset, then [swords] summary
     __shared__ int s_row;
     __shared__ int s_warp[kThreads / 32];
+    constexpr int kRowCap = 2048;  // the CSR row is staged here for the hop-1 tags (longer rows: global)
+    __shared__ int row_s[kRowCap];
     constexpr int kWarps = kThreads / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int swords = (E.words + 31) >> 5;
@@ -284,10 +286,12 @@ __global__ void __launch_bounds__(kThreads) khop2_emit_kernel(const KhopExpand E
             }
         }
         __syncthreads();
+        const int deg = static_cast<int>(ke - kb);
         for (long long k = kb + tid; k < ke; k += kThreads) {  // hop 1 (not every neighbour is 2 hops away)
             const int c = E.nbr[k];
             const int x = c >> 5;
             if (atomicOr(&bits[x], 1u << (c & 31)) == 0u) atomicOr(&summ[x >> 5], 1u << (x & 31));
+            if (deg <= kRowCap) row_s[k - kb] = c;
         }
         __syncthreads();
         if (tid == 0) atomicAnd(&bits[i >> 5], ~(1u << (i & 31)));
@@ -322,6 +326,8 @@ __global__ void __launch_bounds__(kThreads) khop2_emit_kernel(const KhopExpand E
         __syncthreads();
         int pos = incl - cnt + (warp ? s_warp[warp - 1] : 0);
         unsigned* dst = E.ev + (E.ev_off[r] - E.ev_base);
+        const int* rowp = deg <= kRowCap ? row_s : E.nbr + kb;
+        int cur = -1;  // cursor into the CSR row: this thread's columns ascend
         for (int sw = s0; sw < s1; ++sw) {
             unsigned m = summ[sw];
             if (!m) continue;
@@ -335,13 +341,17 @@ __global__ void __launch_bounds__(kThreads) khop2_emit_kernel(const KhopExpand E
                 const unsigned col0 = static_cast<unsigned>(x) << 5;
                 while (v) {
                     const int c = static_cast<int>(col0) + (__ffs(v) - 1);
-                    long long lo = kb, hi = ke;  // hop 1 iff the CSR row lists c
-                    while (lo < hi) {
-                        const long long mid = (lo + hi) >> 1;
-                        if (__ldg(E.nbr + mid) < c) lo = mid + 1;
-                        else hi = mid;
+                    if (cur < 0) {  // first column of this thread: binary search, then advance
+                        int lo = 0, hi = deg;
+                        while (lo < hi) {
+                            const int mid = (lo + hi) >> 1;
+                            if (rowp[mid] < c) lo = mid + 1;
+                            else hi = mid;
+                        }
+                        cur = lo;
                     }
-                    dst[pos++] = (static_cast<unsigned>(c) << 3) | ((lo < ke && __ldg(E.nbr + lo) == c) ? 1u : 2u);
+                    while (cur < deg && rowp[cur] < c) ++cur;
+                    dst[pos++] = (static_cast<unsigned>(c) << 3) | ((cur < deg && rowp[cur] == c) ? 1u : 2u);
                     v &= v - 1;
                 }
             }
