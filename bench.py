@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--kernel", choices=["fastfwd", "replay"], default="fastfwd")
     ap.add_argument("--hop-cap", type=int, default=1,
                     help="distance model: 1 = the reference's (default); 2..7 = opt-in k-hop extension")
+    ap.add_argument("--labels", choices=["sharded", "replicated"], default="sharded",
+                    help="N > 1: labels stay with the rank owning their sigma chunk (counts all-gathered), "
+                         "or are all-gathered to every rank")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
@@ -322,7 +325,10 @@ def run_native(args):
             sweep.ggd(v)
             if record:
                 ev["p3"].record(stream)
-            sweep.gather()
+            if args.labels == "replicated":
+                sweep.gather()
+            else:
+                sweep.gather_counts()
 
     sampler = ClockSampler(local)
     sampler.start()
@@ -330,7 +336,7 @@ def run_native(args):
         step()
     torch.cuda.synchronize(dev)
 
-    per_step, parts = [], {"potentials": [], "alltoall_v": [], "ggd": [], "allgather_labels": []}
+    per_step, parts = [], {"potentials": [], "alltoall_v": [], "ggd": [], "allgather": []}
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -352,7 +358,7 @@ def run_native(args):
         parts["potentials"].append(ev["p0"].elapsed_time(ev["p1"]))
         parts["alltoall_v"].append(ev["p1"].elapsed_time(ev["p2"]))
         parts["ggd"].append(ev["p2"].elapsed_time(ev["p3"]))
-        parts["allgather_labels"].append(ev["p3"].elapsed_time(e1))
+        parts["allgather"].append(ev["p3"].elapsed_time(e1))
     torch.cuda.synchronize(dev)
     wall = time.perf_counter() - t_wall
     sampler.mark(t_epoch0, time.time())
@@ -412,8 +418,9 @@ def run_native(args):
                        "parallelism": f"potentials row-shard x{world}; all-to-all(V) by sigma chunk; "
                                       f"GGD sigma-shard x{world}; all-gather(labels)",
                        "l2": "512 MiB write between timed steps (excluded from the per-step events)",
-                       "step": "potentials(all rows, all sigmas) + exchange V + GGD(succ, centers, labels) "
-                               "+ labels of every sigma on every rank"},
+                       "step": ("potentials(all rows, all sigmas) + exchange V + GGD(succ, centers, labels) + "
+                                + ("labels of every sigma on every rank" if args.labels == "replicated" else
+                                   "every sigma's labels on the rank owning its sigma chunk, counts on every rank"))},
             "breakdown_ms": dict(breakdown, wall_s_timed_region=wall),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,

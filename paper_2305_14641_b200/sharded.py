@@ -175,6 +175,14 @@ class SigmaShardedSweep:
             dist.all_gather_into_tensor(self.nc_full, self.nc, group=self.group)
         return self.ci_full[: self.S], self.nc_full[: self.S]
 
+    def gather_counts(self):
+        """Counts [S] of the whole grid on every rank (enough for the sweep's
+        mutation interval, sweep.cpp:61-71); the labels stay with the rank
+        that owns their sigma chunk (rows [s_begin, s_end) of self.ci)."""
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.nc_full, self.nc, group=self.group)
+        return self.nc_full[: self.S]
+
     def step(self):
         self.potentials()
         v = self.exchange()

@@ -151,9 +151,17 @@ def _worker_sigma(rank, world, port, result_path, n_nodes, sig):
         sweep = sharded.SigmaShardedSweep(g.n, S, rank, world, "cpu", potentials_packed, ggd)
         ci, nc = sweep.step()
         ok = tuple(ci.shape) == (S, g.n) and tuple(nc.shape) == (S,)
-        for q, s in enumerate(sig):
-            _, _, _, cio, ko = O.cluster(g.offsets, g.nbr, g.wt, 10.0, s)
-            ok &= np.array_equal(ci[q].numpy(), cio) and int(nc[q]) == ko
+        ref = [O.cluster(g.offsets, g.nbr, g.wt, 10.0, s) for s in sig]
+        for q in range(S):
+            ok &= np.array_equal(ci[q].numpy(), ref[q][3]) and int(nc[q]) == ref[q][4]
+        # sharded label layout (bench default): counts on every rank, each
+        # rank's own sigma chunk of labels in sweep.ci
+        sweep.potentials()
+        sweep.ggd(sweep.exchange())
+        nc2 = sweep.gather_counts()
+        ok &= [int(x) for x in nc2] == [r[4] for r in ref]
+        for q in range(sweep.s_begin, sweep.s_end):
+            ok &= np.array_equal(sweep.ci[q - sweep.s_begin].numpy(), ref[q][3])
         with open(f"{result_path}.{rank}", "w") as f:
             f.write("ok" if ok else "mismatch")
     finally:
