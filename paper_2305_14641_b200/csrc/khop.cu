@@ -716,30 +716,31 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
         const unsigned* ev_walk = ev_sorted;
         if (emit) {
             F.ev = ev_sorted;  // written in column order
+            // rows whose candidates fit on chip go to the sort kernel (many rows
+            // in flight per SM); the rest to the bitset kernel. With a large
+            // bitset (one block per SM) the 2048-candidate sort size is used
+            // too; with a small one only the 512 size (padding would dominate).
+            cudaMemsetAsync(lens, 0, 4 * sizeof(int), st);
+            khop_split_kernel<<<(nr + 255) / 256, 256, 0, st>>>(ev_off + r0, nr, kSortCap0,
+                                                                 big_emit ? kSortCap1 : kSortCap0, rows0, rows1,
+                                                                 rows2, lens);
+            KhopExpand F0 = F, F1 = F, F2 = F;
+            F0.list = rows0;
+            F0.list_len = lens;
+            F1.list = rows1;
+            F1.list_len = lens + 1;
+            F1.counter = counter + 1;
+            F2.list = rows2;
+            F2.list_len = lens + 2;
+            F2.counter = counter + 2;
+            khop2_sort_kernel<128, 4><<<num_sms() * 8, 128, 0, st>>>(F0, sort_end_bit);
             if (big_emit) {
-                // the bitset holds one row per SM: rows whose candidates fit on
-                // chip go to the sort kernel (many rows in flight), the rest
-                // to the bitset kernel
-                cudaMemsetAsync(lens, 0, 4 * sizeof(int), st);
-                khop_split_kernel<<<(nr + 255) / 256, 256, 0, st>>>(ev_off + r0, nr, kSortCap0, kSortCap1, rows0,
-                                                                     rows1, rows2, lens);
-                KhopExpand F0 = F, F1 = F, F2 = F;
-                F0.list = rows0;
-                F0.list_len = lens;
-                F1.list = rows1;
-                F1.list_len = lens + 1;
-                F1.counter = counter + 1;
-                F2.list = rows2;
-                F2.list_len = lens + 2;
-                F2.counter = counter + 2;
-                khop2_sort_kernel<128, 4><<<num_sms() * 8, 128, 0, st>>>(F0, sort_end_bit);
                 khop2_sort_kernel<256, 8><<<num_sms() * 4, 256, 0, st>>>(F1, sort_end_bit);
                 khop2_emit_kernel<1024><<<std::max(1, std::min(emit_grid, nr)), 1024, edyn, st>>>(F2);
-                count_launch(4);
             } else {
-                khop2_emit_kernel<256><<<std::max(1, std::min(emit_grid, nr)), 256, edyn, st>>>(F);
-                count_launch();
+                khop2_emit_kernel<256><<<std::max(1, std::min(emit_grid, nr)), 256, edyn, st>>>(F2);
             }
+            count_launch(big_emit ? 4 : 3);
         } else {
             khop_expand_kernel<true><<<std::max(1, std::min(grid, nr)), kExpandThreads, dyn, st>>>(F);
             count_launch();
