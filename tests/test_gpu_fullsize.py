@@ -75,3 +75,25 @@ def test_full_graph_ggd_properties_and_sampled_rows(workload):
         check_ggd(off, nbr, v[q], succ[q], res[q].center, res[q].cluster_index, res[q].num_clusters)
         if q in (0, len(sig) - 1):
             assert sampled_rows_match(off, nbr, v[q], s, rows), f"sigma {s}"
+
+
+def test_khop_full_lfr_sampled_rows_and_ggd_properties():
+    """k-hop extension (hop cap 2) on the 1M-node LFR graph: ~1.3G hop-2
+    events through every emission path (on-chip sort, bitset kernel)."""
+    from bench_tools import graphgen
+    graphgen.build()
+    off, nbr = graphgen.lfr()
+    n = len(off) - 1
+    sig = np.array([1.0, 4.0, 30.0])
+    N.set_hop_cap(2)
+    try:
+        res, v, succ = N.cluster_sweep(N.Csr(off, nbr, None, 10.0), sig, want_v=True, want_succ=True)
+    finally:
+        N.set_hop_cap(1)
+    deg = np.diff(off)
+    rows = np.unique(np.concatenate([[0, n - 1], np.argsort(deg)[-2:], np.argsort(deg)[:2],
+                                     np.arange(11, n, n // 12)])).astype(np.int32)
+    for q, s in enumerate(sig):
+        check_ggd(off, nbr, v[q], succ[q], res[q].center, res[q].cluster_index, res[q].num_clusters)
+        ref = O.potentials_khop(off, nbr, None, 10.0, s, 2, workers=16, rows=rows)
+        assert np.array_equal(v[q][rows].view(np.int64), ref.view(np.int64)), f"sigma {s}"
