@@ -131,8 +131,10 @@ gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_s
 /* All pointers in gqc_csr and the buffers below are device pointers on the
  * current device; `stream` is a cudaStream_t (NULL = legacy default stream).
  * sigmas stays a host array (the per-sigma exp constants are a host concern).
- * Nothing is synchronized: errors from the kernels surface at the caller's
- * next synchronization. */
+ * Nothing is synchronized (except with GQC_OPT_HOP_CAP > 1, where a
+ * potential launch reads the per-row event counts back once to size its
+ * batches): errors from the kernels surface at the caller's next
+ * synchronization. */
 
 /* Potentials of rows [row_begin, row_end) for all sigmas, node-major:
  * v_rows[(i - row_begin) * n_sigma + k]. Row shards of a multi-GPU sweep. */

@@ -680,25 +680,26 @@ int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTabl
                                                   static_cast<int*>(nullptr), static_cast<const int*>(nullptr),
                                                   static_cast<int*>(nullptr), nr);
         const std::size_t b_ev = bytes_of(std::max<long long>(items, 1) * sizeof(unsigned));
+        const std::size_t b_raw = emit ? 0 : b_ev;  // ordered emission writes the final list directly
         const std::size_t b_seg = 2 * bytes_of((nr + 1) * sizeof(int));
         const std::size_t b_key = bytes_of(nr * sizeof(int));
         void* bm = nullptr;
-        if ((e = cudaMallocFromPoolAsync(&bm, 2 * b_ev + b_seg + 7 * b_key + bytes_of(sort_bytes) +
+        if ((e = cudaMallocFromPoolAsync(&bm, b_raw + b_ev + b_seg + 7 * b_key + (emit ? 0 : bytes_of(sort_bytes)) +
                                                   bytes_of(key_bytes) + 512,
                                          pool, st)) != cudaSuccess)
             return e;
         char* q = static_cast<char*>(bm);
-        unsigned* ev_raw = reinterpret_cast<unsigned*>(q);
-        unsigned* ev_sorted = reinterpret_cast<unsigned*>(q + b_ev);
-        int* seg_b = reinterpret_cast<int*>(q + 2 * b_ev);
+        unsigned* ev_raw = reinterpret_cast<unsigned*>(q);  // (unused with ordered emission)
+        unsigned* ev_sorted = reinterpret_cast<unsigned*>(q + b_raw);
+        int* seg_b = reinterpret_cast<int*>(q + b_raw + b_ev);
         int* seg_e = seg_b + b_seg / (2 * sizeof(int));
-        int* key_in = reinterpret_cast<int*>(q + 2 * b_ev + b_seg);
+        int* key_in = reinterpret_cast<int*>(q + b_raw + b_ev + b_seg);
         int* key_out = key_in + b_key / sizeof(int);
         int* id_in = key_out + b_key / sizeof(int);
         int* id_out = id_in + b_key / sizeof(int);
-        int* wcounter = reinterpret_cast<int*>(q + 2 * b_ev + b_seg + 4 * b_key);
-        void* sort_tmp = q + 2 * b_ev + b_seg + 4 * b_key + 256;
-        void* key_tmp = static_cast<char*>(sort_tmp) + bytes_of(sort_bytes);
+        int* wcounter = reinterpret_cast<int*>(q + b_raw + b_ev + b_seg + 4 * b_key);
+        void* sort_tmp = q + b_raw + b_ev + b_seg + 4 * b_key + 256;
+        void* key_tmp = static_cast<char*>(sort_tmp) + (emit ? 0 : bytes_of(sort_bytes));
         int* rows0 = reinterpret_cast<int*>(static_cast<char*>(key_tmp) + bytes_of(key_bytes));
         int* rows1 = rows0 + b_key / sizeof(int);
         int* rows2 = rows1 + b_key / sizeof(int);
