@@ -44,4 +44,16 @@ sc = torch.empty((w.n, S), dtype=torch.int32, device="cuda"); N.dev_successors(d
 c = torch.empty((S, w.n), dtype=torch.int32, device="cuda"); ci = torch.empty_like(c); nc = torch.empty(S, dtype=torch.int32, device="cuda")
 ws = torch.empty(N.dev_resolve_workspace(w.n, S), dtype=torch.uint8, device="cuda")
 N.dev_resolve(w.n, S, sc, c, ci, nc, ws); torch.cuda.synchronize()
+# k-hop extension: hop cap 2 (on-chip sort + bitset emission: a row with > 512
+# candidates) and 3 (expand + segmented sort), odd N
+u = H.random_graph(1201, 9.0, seed=5, unit=True)
+star_rows = np.arange(1, 700, dtype=np.int32)
+kh = H.G(1201, np.concatenate([u.nbr[:0], np.zeros(699, np.int32)]), star_rows)
+for gg in (u, kh):
+    for K in (2, 3):
+        N.set_hop_cap(K)
+        got = N.potentials(gg.csr(N), [0.9, 6.0])
+        for q, s in enumerate([0.9, 6.0]):
+            check(got[q], O.potentials_khop(gg.offsets, gg.nbr, gg.wt, 10.0, s, K))
+N.set_hop_cap(1)
 print("sanitize smoke ok")
