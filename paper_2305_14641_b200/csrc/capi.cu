@@ -128,6 +128,8 @@ struct DeviceCtx {
     DevBuf off, nbr, w, v_nm, v_sm, succ, center, ci, nc, ws, tail, entry;
     int* nc_host = nullptr;  // pinned staging for per-sigma counts (cudaHostAlloc)
     int nc_host_cap = 0;
+    DevBuf slab_sync;            // polled upload: [4] slab flags, [4] error word
+    int* slab_host = nullptr;    // pinned: [0..3] = 1 (flag sources), [4] error readback
 };
 
 // Device->host copies into pageable memory block the calling thread until
@@ -239,9 +241,15 @@ void host_exp_table(const double* d2, long long count, const std::vector<double>
 // Potentials of rows [row_begin, row_end) into v_nm[(i-row_begin)*S + s]
 // (device), for a device-resident CSR. host_w: the same weights on the host
 // (only consulted for weighted graphs), or nullptr to fetch what is needed.
+struct SlabSync {  // polled CSR upload (see PotentialLaunch::slab_flags)
+    const int* flags = nullptr;
+    int bound[5] = {};
+    int* err = nullptr;
+};
+
 void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S, int row_begin, int row_end,
                     double* v_nm, const double* host_w, cudaStream_t st, const std::int64_t* host_off = nullptr,
-                    int out_chunk = 0, long long out_chunk_stride = 0) {
+                    int out_chunk = 0, long long out_chunk_stride = 0, const SlabSync* sync = nullptr) {
     const int n = g.n;
     const int mode = g_opt.exp_mode;
     const bool weighted = g.w != nullptr;
@@ -307,6 +315,11 @@ void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S,
         P.out_chunk = out_chunk > 0 ? out_chunk : S;  // packed sigma chunks, or plain rows of S
         P.out_ld = P.out_chunk;
         P.out_chunk_stride = out_chunk > 0 ? out_chunk_stride : 0;
+        if (sync) {
+            P.slab_flags = sync->flags;
+            for (int k = 0; k < 5; ++k) P.slab_bound[k] = sync->bound[k];
+            P.slab_err = sync->err;
+        }
         std::vector<double> neg_inv(Sc);
         for (int s = 0; s < Sc; ++s) {
             P.c[s] = make_sigma_consts(sigmas[s0 + s], g.W, mode);
@@ -394,6 +407,14 @@ struct ClassOrderScope {
     }
     const ClassOrder* get() const { return co.dir ? &co : nullptr; }
 };
+
+bool polled_upload_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("GQC_POLLED_UPLOAD");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
 
 bool class_order_enabled() {
     static const bool on = [] {
@@ -623,13 +644,55 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
         }
         // (k-hop rows read their neighbours' rows too: one slab, the whole CSR)
         const int slabs = (nnz >= (1 << 20) && g_opt.hop_cap == 1) ? 4 : 1;
+        const bool polled = slabs == 4 && !weighted && n_sigma >= 8 && polled_upload_enabled();
         std::vector<int> bound(slabs + 1, n);
         bound[0] = 0;
-        for (int k = 1; k < slabs; ++k)  // equal-nnz row slabs
-            bound[k] = static_cast<int>(std::lower_bound(g->offsets, g->offsets + n + 1, nnz * k / slabs) - g->offsets);
+        // equal-nnz row slabs; polled: growing (cumulative 10%, 30%, 60%): the
+        // first slab lands fast and every later one (the copy engine moves
+        // the CSR ~2.7x faster than the kernel consumes it) arrives before
+        // the warps reach it
+        static const double kGeo[3] = {0.10, 0.30, 0.60};
+        for (int k = 1; k < slabs; ++k) {
+            const long long at = polled ? static_cast<long long>(nnz * kGeo[k - 1]) : nnz * k / slabs;
+            bound[k] = static_cast<int>(std::lower_bound(g->offsets, g->offsets + n + 1, at) - g->offsets);
+        }
         const std::size_t cells = static_cast<std::size_t>(n) * n_sigma;
         double* v_nm = C.v_nm.get<double>(cells);
-        for (int k = 0; k < slabs; ++k) {
+        // Polled upload (unit weights, warp kernel; GQC_POLLED_UPLOAD=0 turns
+        // it off): ONE potential launch starts once the offsets are resident;
+        // its warps take rows slab-major and wait on a flag per slab that the
+        // copy stream sets right after the slab's entries land. Each slab's
+        // copy is extended to whole 128 B lines so no line a warp reads can be
+        // cached half-written. Otherwise one launch per slab on its own stream.
+        if (polled) {
+            int* flags = C.slab_sync.get<int>(8);
+            if (!C.slab_host) {
+                cuda_check(cudaHostAlloc(&C.slab_host, 8 * sizeof(int), cudaHostAllocDefault), "cudaHostAlloc");
+                for (int k = 0; k < 8; ++k) C.slab_host[k] = 1;
+            }
+            C.slab_host[4] = 0;
+            cuda_check(cudaMemsetAsync(flags, 0, 8 * sizeof(int), cs), "clear flags");
+            cuda_check(cudaEventRecord(C.ev[0], cs), "event");  // offsets (and the flags) resident
+            for (int k = 0; k < slabs; ++k) {
+                const long long a = g->offsets[bound[k]], b = g->offsets[bound[k + 1]];
+                const long long a2 = a & ~31ll, b2 = std::min<long long>(nnz, (b + 31) & ~31ll);
+                if (b2 > a2)
+                    cuda_check(cudaMemcpyAsync(nbr + a2, g->nbr + a2, (b2 - a2) * sizeof(std::int32_t),
+                                               cudaMemcpyHostToDevice, cs),
+                               "copy nbr");
+                cuda_check(cudaMemcpyAsync(flags + k, C.slab_host + k, sizeof(int), cudaMemcpyHostToDevice, cs),
+                           "set slab flag");
+            }
+            cuda_check(cudaStreamWaitEvent(st, C.ev[0], 0), "wait");
+            SlabSync sync;
+            sync.flags = flags;
+            for (int k = 0; k <= slabs; ++k) sync.bound[k] = bound[k];
+            sync.err = flags + 4;
+            run_potentials(C, d, sigmas, n_sigma, 0, n, v_nm, nullptr, st, g->offsets, 0, 0, &sync);
+            cuda_check(cudaMemcpyAsync(C.slab_host + 4, flags + 4, sizeof(int), cudaMemcpyDeviceToHost, st),
+                       "copy upload status");
+        }
+        for (int k = 0; k < slabs && !polled; ++k) {
             const long long a = g->offsets[bound[k]], b = g->offsets[bound[k + 1]];
             if (b > a) {
                 cuda_check(cudaMemcpyAsync(nbr + a, g->nbr + a, (b - a) * sizeof(std::int32_t), cudaMemcpyHostToDevice, cs),
@@ -648,7 +711,7 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
                                weighted ? g->w : nullptr, ss, g->offsets);
             cuda_check(cudaEventRecord(C.slab_done[k], ss), "event");
         }
-        for (int k = 0; k < slabs; ++k) cuda_check(cudaStreamWaitEvent(st, C.slab_done[k], 0), "wait");
+        for (int k = 0; k < slabs && !polled; ++k) cuda_check(cudaStreamWaitEvent(st, C.slab_done[k], 0), "wait");
         tr.mark("potentials");
         double* v_src = v_nm;
         const bool v_early = v_out && host_pinned(v_out);  // pageable: copied after the GGD launches
@@ -730,6 +793,7 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
         tr.mark("downloads");
         cuda_check(cudaStreamSynchronize(cs), "cluster sweep (copies)");
         cuda_check(cudaStreamSynchronize(st), "cluster sweep");
+        if (polled && C.slab_host[4]) fail(GQC_ECUDA, "CSR upload did not arrive (polled slab flag timeout)");
         std::copy(nc_stage, nc_stage + n_sigma, num_clusters_out);
     }
 }

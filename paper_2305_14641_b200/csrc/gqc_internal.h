@@ -51,6 +51,13 @@ struct PotentialLaunch {
     std::int32_t out_ld, out_col0;
     std::int32_t out_chunk;
     long long out_chunk_stride;
+    // Polled CSR upload (host pipeline, unit weights, warp kernel): rows
+    // [slab_bound[k], slab_bound[k+1]) may be read once slab_flags[k] != 0
+    // (set by a copy after the slab's data on the copy stream); rows are
+    // scheduled slab-major. slab_err: set if a flag never arrives (timeout).
+    const int* slab_flags;
+    std::int32_t slab_bound[5];
+    int* slab_err;
     SigmaConsts c[kMaxSigmaPerLaunch];
 };
 

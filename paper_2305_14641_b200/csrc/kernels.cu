@@ -153,11 +153,15 @@ constexpr int kRowsPerGrab = 2;
 constexpr int kHeavyDegree = 128;  // GGD argmin: rows above this degree use a block each
 
 __global__ void row_degree_kernel(const long long* __restrict__ off, int row_begin, int rows, int* __restrict__ deg,
-                                  int* __restrict__ id) {
+                                  int* __restrict__ id, const int* __restrict__ slab_flags, int b1, int b2, int b3) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= rows) return;
     const int i = row_begin + k;
     deg[k] = static_cast<int>(off[i + 1] - off[i]);
+    if (slab_flags) {  // polled upload: slab-major (earlier slabs first), heaviest first inside a slab
+        const int slab = (i >= b1) + (i >= b2) + (i >= b3);
+        deg[k] = ((3 - slab) << 24) | min(deg[k], (1 << 24) - 1);
+    }
     id[k] = i;
 }
 
@@ -337,6 +341,32 @@ constexpr int kPrefixStride = kPrefixCap + 1;
 #endif
 constexpr int kBatchMinDegree = GQC_BATCH_MIN_DEGREE;  // padded: no bank conflicts across lanes
 
+// Polled CSR upload: lane 0 waits (acquire) until the copy stream has set
+// the flag of row i's slab; a flag that never arrives sets *slab_err after
+// ~5 s instead of hanging the GPU.
+__device__ __noinline__ void wait_slab(const int* flags, const int b1, const int b2, const int b3, int* err,
+                                       const int i) {
+    const int slab = (i >= b1) + (i >= b2) + (i >= b3);
+    if ((threadIdx.x & 31) == 0) {
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+            int f;
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(flags + slab) : "memory");
+            if (f || *static_cast<volatile int*>(err)) break;  // arrived, or another warp timed out
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 5000000000ull) {
+                atomicExch(err, 1);
+                break;
+            }
+            __nanosleep(256);
+        }
+    }
+    __syncwarp();
+    __threadfence();
+}
+
 template <bool kFF, int kW>
 __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp_kernel(const __grid_constant__ PotentialLaunch P,
                                                                 const PrefixTable T, const RowSched R) {
@@ -446,6 +476,7 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
         const int i = R.order[grab];
         ++grab;
         --left;
+        if (P.slab_flags) wait_slab(P.slab_flags, P.slab_bound[1], P.slab_bound[2], P.slab_bound[3], P.slab_err, i);
         const long long kbeg = P.offsets[i], kend = P.offsets[i + 1];
         Chain num, den;
         num.s = 0.0; num.top = 0.0; num.inc = 0.0; num.f_tie = tie_num; num.flags = 0;
@@ -1051,7 +1082,8 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
         int* counter = reinterpret_cast<int*>(b + 4 * arr);
         void* temp = b + 4 * arr + 256;
         row_degree_kernel<<<grid_for(rows), kBlock, 0, st>>>(reinterpret_cast<const long long*>(p.offsets),
-                                                              p.row_begin, rows, deg_in, id_in);
+                                                              p.row_begin, rows, deg_in, id_in, p.slab_flags,
+                                                              p.slab_bound[1], p.slab_bound[2], p.slab_bound[3]);
         count_launch();
         e = cub::DeviceRadixSort::SortPairsDescending(temp, sort_bytes, deg_in, deg_out, id_in, id_out, rows, 0, 32, st);
         count_launch(2);
