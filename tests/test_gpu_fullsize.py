@@ -64,7 +64,9 @@ def test_full_graph_ggd_properties_and_sampled_rows(workload):
     graphgen.build()
     off, nbr = graphgen.lfr() if workload == "lfr1m" else graphgen.rmat()
     grid = np.asarray(log_sigma_grid(10.0, 32))
-    picks = [0, 9, 17, 31] if workload == "lfr1m" else [0, 31]
+    # LFR: 8 sigmas -> the host pipeline's polled CSR upload (one launch
+    # waiting on per-slab flags); R-MAT: 2 sigmas -> the per-slab launches
+    picks = [0, 5, 9, 13, 17, 21, 26, 31] if workload == "lfr1m" else [0, 31]
     sig = grid[picks]
     csr = N.Csr(off, nbr, None, 10.0)
     res, v, succ = N.cluster_sweep(csr, sig, want_v=True, want_succ=True)
