@@ -416,7 +416,9 @@ def run_native(args):
                        "distance": ("reference (graph.cpp:258-267, hop cap 1)" if args.hop_cap == 1 else
                                     f"k-hop extension, hop cap {args.hop_cap} (not a reference feature)"),
                        "parallelism": f"potentials row-shard x{world}; all-to-all(V) by sigma chunk; "
-                                      f"GGD sigma-shard x{world}; all-gather(labels)",
+                                      f"GGD sigma-shard x{world}; "
+                                      + ("all-gather(labels, counts)" if args.labels == "replicated"
+                                         else "all-gather(counts), labels sharded by sigma"),
                        "l2": "512 MiB write between timed steps (excluded from the per-step events)",
                        "step": ("potentials(all rows, all sigmas) + exchange V + GGD(succ, centers, labels) + "
                                 + ("labels of every sigma on every rank" if args.labels == "replicated" else
