@@ -127,6 +127,16 @@ gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_s
                              int32_t* succ_out, int32_t* center_out, int32_t* cluster_index_out,
                              int32_t* num_clusters_out);
 
+/* gqc_cluster_sweep plus, per sigma, intra_out[k] = the number of CSR
+ * entries (i, j) with cluster_index[k][i] == cluster_index[k][j]: the
+ * intra-cluster weight of modularity (metrics.cpp:37-44) for a unit-weight
+ * graph, exact, so the host evaluates modularity in O(N + K) instead of
+ * O(nnz). Weighted graphs -> GQC_EINVAL ("intra counts need unit weights").
+ * intra_out may be NULL (then identical to gqc_cluster_sweep). */
+gqc_status gqc_cluster_sweep_intra(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out,
+                                   int32_t* succ_out, int32_t* center_out, int32_t* cluster_index_out,
+                                   int32_t* num_clusters_out, int64_t* intra_out);
+
 /* -------------------------------------------------------------- device API */
 /* All pointers in gqc_csr and the buffers below are device pointers on the
  * current device; `stream` is a cudaStream_t (NULL = legacy default stream).

@@ -125,7 +125,7 @@ struct DeviceCtx {
     cudaEvent_t ev[16] = {};
     cudaEvent_t slab_done[4] = {};
     cudaMemPool_t pool = nullptr;  // stream-ordered scratch that keeps its memory
-    DevBuf off, nbr, w, v_nm, v_sm, succ, center, ci, nc, ws, tail, entry;
+    DevBuf off, nbr, w, v_nm, v_sm, succ, center, ci, nc, ws, tail, entry, intra;
     int* nc_host = nullptr;  // pinned staging for per-sigma counts (cudaHostAlloc)
     int nc_host_cap = 0;
     DevBuf slab_sync;            // polled upload: [4] slab flags, [4] error word
@@ -459,7 +459,7 @@ int32_t gqc_device_count(void) {
 
 static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out,
                                int32_t* succ_out, int32_t* center_out, int32_t* cluster_index_out,
-                               int32_t* num_clusters_out);
+                               int32_t* num_clusters_out, int64_t* intra_out = nullptr);
 
 gqc_status gqc_init(void) {
     return guarded([&] {
@@ -605,7 +605,8 @@ constexpr int kGgdChunk = GQC_GGD_CHUNK;
 
 // The body of gqc_cluster_sweep (callers hold g_mu).
 static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out, int32_t* succ_out,
-                        int32_t* center_out, int32_t* cluster_index_out, int32_t* num_clusters_out) {
+                        int32_t* center_out, int32_t* cluster_index_out, int32_t* num_clusters_out,
+                        int64_t* intra_out) {
     {
         check_sigmas(sigmas, n_sigma);
         check_csr_shape(g);
@@ -618,6 +619,7 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
         const long long nnz = g->nnz;
         const bool weighted = g->w && !all_unit(g->w, nnz);
         if (g_opt.hop_cap > 1 && weighted) fail(GQC_EINVAL, "k-hop distances need unit weights");
+        if (intra_out && weighted) fail(GQC_EINVAL, "intra counts need unit weights");
 
         // Pipeline: the CSR goes up in row slabs on the copy stream while the
         // compute stream runs the potentials of the slabs already resident
@@ -730,6 +732,7 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
         int* dc = C.center.get<int>(cells);
         int* dci = C.ci.get<int>(cells);
         int* dnc = C.nc.get<int>(n_sigma);
+        long long* d_intra = intra_out ? C.intra.get<long long>(n_sigma) : nullptr;
         const std::size_t wsb = labels_workspace_bytes(n, n_sigma);
         void* ws = C.ws.get<char>(wsb);
         // GGD chunk boundaries: equal chunks of GQC_GGD_CHUNK sigmas (16), or
@@ -771,6 +774,8 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
                        "successor kernel");
             cuda_check(launch_chase(n, Sc, ds + o, dc + o, st, ws), "chase kernel");
             cuda_check(launch_labels(n, Sc, dc + o, dci + o, dnc + s0, ws, wsb, st, true), "label kernels");
+            if (intra_out)
+                cuda_check(launch_intra_counts(n, Sc, d.offsets, d.nbr, dci + o, d_intra + s0, st), "intra counts");
             tr.mark("ggd_chunk");
             if (overlap) {
                 cudaEvent_t e = C.ev[ev_i];
@@ -791,6 +796,9 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
         cuda_check(cudaEventRecord(C.ev[8], cs), "event");
         cuda_check(cudaStreamWaitEvent(st, C.ev[8], 0), "wait");
         tr.mark("downloads");
+        if (intra_out)
+            cuda_check(cudaMemcpyAsync(intra_out, d_intra, n_sigma * sizeof(long long), cudaMemcpyDeviceToHost, st),
+                       "copy intra counts");
         cuda_check(cudaStreamSynchronize(cs), "cluster sweep (copies)");
         cuda_check(cudaStreamSynchronize(st), "cluster sweep");
         if (polled && C.slab_host[4]) fail(GQC_ECUDA, "CSR upload did not arrive (polled slab flag timeout)");
@@ -803,6 +811,15 @@ gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_s
                              int32_t* num_clusters_out) {
     return guarded([&] {
         cluster_sweep_impl(g, sigmas, n_sigma, v_out, succ_out, center_out, cluster_index_out, num_clusters_out);
+    });
+}
+
+gqc_status gqc_cluster_sweep_intra(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out,
+                                   int32_t* succ_out, int32_t* center_out, int32_t* cluster_index_out,
+                                   int32_t* num_clusters_out, int64_t* intra_out) {
+    return guarded([&] {
+        cluster_sweep_impl(g, sigmas, n_sigma, v_out, succ_out, center_out, cluster_index_out, num_clusters_out,
+                           intra_out);
     });
 }
 

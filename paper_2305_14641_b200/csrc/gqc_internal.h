@@ -89,6 +89,10 @@ int launch_successors(std::int32_t n, const std::int64_t* offsets, const std::in
                       std::int32_t ld, std::int32_t s0, std::int32_t n_sigma, std::int32_t row_begin,
                       std::int32_t row_end, std::int32_t* out, long long out_row, long long out_col, long long nnz,
                       void* pool, void* stream, const ClassOrder* co = nullptr);
+// out[s] = CSR entries (i, j) whose cluster_index matches for sigma s (device,
+// sigma-major labels [n_sigma][n]); the unit-weight modularity intra term.
+int launch_intra_counts(std::int32_t n, std::int32_t n_sigma, const std::int64_t* offsets, const std::int32_t* nbr,
+                        const std::int32_t* ci_sm, long long* out, void* stream);
 int launch_transpose_i32(const std::int32_t* in, std::int32_t n, std::int32_t n_sigma, std::int32_t* out, void* stream);
 // labels_workspace (optional): launch_labels' workspace; the chase then writes
 // the center flags there and launch_labels must be called with flags_ready.

@@ -1325,6 +1325,36 @@ int launch_class_order(int n, const std::int64_t* offsets, long long nnz, const 
     return cudaGetLastError();
 }
 
+namespace {
+// Modularity's intra-cluster weight for unit weights (metrics.cpp:37-44):
+// out[s] += #{CSR entries (i, j) with ci[s][i] == ci[s][j]}, an exact integer
+// (the reference sums 1.0s, also exact). Thread per row, blockIdx.y = sigma.
+__global__ void __launch_bounds__(kBlock) intra_count_kernel(const long long* __restrict__ off,
+                                                             const int* __restrict__ nbr,
+                                                             const int* __restrict__ ci, int n,
+                                                             unsigned long long* __restrict__ out) {
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    const int* c = ci + static_cast<long long>(blockIdx.y) * n;
+    unsigned long long cnt = 0;
+    if (i < n) {
+        const int ci_i = c[i];
+        for (long long k = off[i]; k < off[i + 1]; ++k) cnt += __ldg(c + __ldg(nbr + k)) == ci_i;
+    }
+    for (int d = 16; d; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out + blockIdx.y, cnt);
+}
+}  // namespace
+
+int launch_intra_counts(int n, int n_sigma, const std::int64_t* offsets, const std::int32_t* nbr,
+                        const std::int32_t* ci_sm, long long* out, void* stream) {
+    auto st = static_cast<cudaStream_t>(stream);
+    cudaMemsetAsync(out, 0, n_sigma * sizeof(long long), st);
+    intra_count_kernel<<<dim3(grid_for(n), n_sigma), kBlock, 0, st>>>(
+        reinterpret_cast<const long long*>(offsets), nbr, ci_sm, n, reinterpret_cast<unsigned long long*>(out));
+    count_launch();
+    return cudaGetLastError();
+}
+
 int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nbr, const double* v, int ld, int s0,
                       int n_sigma, int row_begin, int row_end, std::int32_t* out, long long out_row, long long out_col,
                       long long nnz, void* pool, void* stream, const ClassOrder* co) {

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <optional>
 #include <span>
 #include <vector>
 
@@ -20,6 +21,10 @@ struct ClusterAssignment {
     std::vector<std::int32_t> cluster_index;
     std::vector<std::int32_t> centers;
     std::int32_t num_clusters = 0;
+    // Extension (not in the reference struct): modularity's intra-cluster
+    // weight of a unit-weight graph, counted on the device by cluster_batch
+    // (exact); modularity() then skips its O(nnz) row loop.
+    std::optional<double> intra_weight;
 };
 
 SuccessorMap build_successors(const Graph& g, const PotentialField& pf);

@@ -49,17 +49,22 @@ std::vector<ClusterAssignment> cluster_batch(const Graph& g, std::span<const dou
     // bounded host staging: 64 sigmas per device call
     constexpr std::size_t kChunk = 64;
     std::vector<std::int32_t> center, ci, k;
+    std::vector<std::int64_t> intra;
+    const bool unit = c.w == nullptr;  // modularity's intra term comes back exact with the labels
     for (std::size_t q0 = 0; q0 < sigmas.size(); q0 += kChunk) {
         const std::size_t m = std::min(kChunk, sigmas.size() - q0);
         center.resize(with_center ? m * n : 0);
         ci.resize(m * n);
         k.resize(m);
-        detail::check(gqc_cluster_sweep(&c, sigmas.data() + q0, static_cast<std::int32_t>(m), nullptr, nullptr,
-                                        with_center ? center.data() : nullptr, ci.data(), k.data()));
+        intra.resize(unit ? m : 0);
+        detail::check(gqc_cluster_sweep_intra(&c, sigmas.data() + q0, static_cast<std::int32_t>(m), nullptr, nullptr,
+                                              with_center ? center.data() : nullptr, ci.data(), k.data(),
+                                              unit ? intra.data() : nullptr));
         for (std::size_t q = 0; q < m; ++q) {
             ClusterAssignment& a = out[q0 + q];
             a.cluster_index.assign(ci.begin() + q * n, ci.begin() + (q + 1) * n);
             a.num_clusters = k[q];
+            if (unit) a.intra_weight = static_cast<double>(intra[q]);
             if (with_center) {
                 a.center.assign(center.begin() + q * n, center.begin() + (q + 1) * n);
                 a.centers = centers_of(a.center);

@@ -78,6 +78,7 @@ def _load():
         "gqc_build_successors": [P, P, P],
         "gqc_resolve_centers": [i32, P, P, P, P],
         "gqc_cluster_sweep": [P, P, i32, P, P, P, P, P],
+        "gqc_cluster_sweep_intra": [P, P, i32, P, P, P, P, P, P],
         "gqc_dev_potentials": [P, P, i32, i32, i32, P, P],
         "gqc_dev_potentials_packed": [P, P, i32, i32, i32, P, i32, i64, P],
         "gqc_dev_ggd": [P, P, i32, P, P, P, P, P, C.c_size_t, P],
@@ -270,6 +271,19 @@ def cluster_sweep_raw(g: Csr, sigmas: np.ndarray, center: Optional[np.ndarray], 
     cs = g.c_struct()
     _check(_lib.gqc_cluster_sweep(C.byref(cs), _ptr(sigmas), len(sigmas), _ptr(v), _ptr(succ), _ptr(center),
                                   _ptr(ci), _ptr(k)))
+
+
+def cluster_sweep_intra(g: Csr, sigmas: Sequence[float]):
+    """Labels, counts and modularity's intra-cluster weight per sigma
+    (gqc_cluster_sweep_intra; unit-weight graphs)."""
+    s = np.ascontiguousarray(np.atleast_1d(np.asarray(sigmas, dtype=np.float64)))
+    ci = np.empty((len(s), g.n), dtype=np.int32)
+    k = np.zeros(len(s), dtype=np.int32)
+    intra = np.zeros(len(s), dtype=np.int64)
+    cs = g.c_struct()
+    _check(_lib.gqc_cluster_sweep_intra(C.byref(cs), _ptr(s), len(s), None, None, None, _ptr(ci), _ptr(k),
+                                        _ptr(intra)))
+    return ci, k, intra
 
 
 def cluster_sweep(g: Csr, sigmas: Sequence[float], want_v: bool = False, want_succ: bool = False,

@@ -578,3 +578,22 @@ print(json.dumps(out))
     res, v, succ = N.cluster_sweep(g.csr(N), sig, want_v=True, want_succ=True)
     for q in (0, 9, 31):
         assert np.array_equal(succ[q], O.build_successors(g.offsets, g.nbr, v[q]))
+
+
+def test_cluster_sweep_intra_counts():
+    """gqc_cluster_sweep_intra: modularity's intra-cluster weight per sigma
+    (metrics.cpp:37-44) counted on the device, equal to a numpy count over
+    the CSR, and the oracle's modularity from those labels; weighted graphs
+    are refused."""
+    off, nbr = H.sbm_csr()
+    csr = N.Csr(off, nbr, None, 10.0)
+    sig = O.log_sigma_grid(10.0, 32)
+    ci, k, intra = N.cluster_sweep_intra(csr, sig)
+    res, _, _ = N.cluster_sweep(csr, sig)
+    rows = np.repeat(np.arange(len(off) - 1), np.diff(off))
+    for q in (0, 7, 19, 31):
+        assert np.array_equal(ci[q], res[q].cluster_index) and k[q] == res[q].num_clusters
+        assert intra[q] == int(np.count_nonzero(ci[q][rows] == ci[q][nbr]))
+    w = H.random_graph(300, 5, 3, unit=False)
+    with pytest.raises(ValueError, match="intra counts need unit weights"):
+        N.cluster_sweep_intra(w.csr(N), [1.0])
