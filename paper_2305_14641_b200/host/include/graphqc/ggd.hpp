@@ -23,9 +23,15 @@ struct ClusterAssignment {
     std::int32_t num_clusters = 0;
     // Extension (not in the reference struct): modularity's intra-cluster
     // weight of a unit-weight graph, counted on the device by cluster_batch
-    // (exact); modularity() then skips its O(nnz) row loop.
+    // (exact); modularity() then skips its O(nnz) row loop — only while
+    // cluster_index still hashes to intra_labels_hash (edited labels fall
+    // back to the full loop).
     std::optional<double> intra_weight;
+    std::uint64_t intra_labels_hash = 0;
 };
+
+// Hash of a labelling that guards ClusterAssignment::intra_weight.
+std::uint64_t labels_hash(const std::vector<std::int32_t>& labels);
 
 SuccessorMap build_successors(const Graph& g, const PotentialField& pf);
 ClusterAssignment resolve_centers(const SuccessorMap& s);

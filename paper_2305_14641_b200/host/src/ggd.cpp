@@ -64,7 +64,10 @@ std::vector<ClusterAssignment> cluster_batch(const Graph& g, std::span<const dou
             ClusterAssignment& a = out[q0 + q];
             a.cluster_index.assign(ci.begin() + q * n, ci.begin() + (q + 1) * n);
             a.num_clusters = k[q];
-            if (unit) a.intra_weight = static_cast<double>(intra[q]);
+            if (unit) {
+                a.intra_weight = static_cast<double>(intra[q]);
+                a.intra_labels_hash = labels_hash(a.cluster_index);
+            }
             if (with_center) {
                 a.center.assign(center.begin() + q * n, center.begin() + (q + 1) * n);
                 a.centers = centers_of(a.center);
@@ -72,6 +75,16 @@ std::vector<ClusterAssignment> cluster_batch(const Graph& g, std::span<const dou
         }
     }
     return out;
+}
+
+std::uint64_t labels_hash(const std::vector<std::int32_t>& labels) {
+    std::uint64_t h = 0x9E3779B97F4A7C15ull ^ labels.size();
+    for (std::int32_t x : labels) {
+        h ^= static_cast<std::uint32_t>(x);
+        h *= 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 29;
+    }
+    return h;
 }
 
 ClusterAssignment cluster(const Graph& g, double sigma, int workers) {  // ggd.cpp:59-62

@@ -9,6 +9,7 @@
 #include <tuple>
 
 #include "graphqc/format.hpp"
+#include "graphqc/ggd.hpp"
 #include "graphqc/graph.hpp"
 #include "graphqc/metrics.hpp"
 #include "graphqc/sweep.hpp"
@@ -75,6 +76,23 @@ int main(int argc, char** argv) {
     {
         Graph g = from_text("a a\na b\n");
         CHECK(g.num_nodes() == 2 && g.num_edges() == 1 && neighbors(g, 0).size() == 1);
+    }
+    // modularity with a device intra count (ClusterAssignment::intra_weight):
+    // used only while the labels still hash to what was counted
+    {
+        Graph g = from_text("0 1\n1 2\n2 0\n3 4\n4 5\n5 3\n2 3\n");
+        ClusterAssignment a;
+        a.cluster_index = {0, 0, 0, 1, 1, 1};
+        a.num_clusters = 2;
+        const double plain = modularity(g, a);
+        a.intra_weight = 12.0;  // the true count of equal-label CSR entries
+        a.intra_labels_hash = labels_hash(a.cluster_index);
+        CHECK(modularity(g, a) == plain);
+        a.intra_weight = 999.0;  // a stale count for edited labels is ignored
+        a.cluster_index[3] = 0;
+        ClusterAssignment b = a;
+        b.intra_weight.reset();
+        CHECK(modularity(g, a) == modularity(g, b));
     }
     // parse errors carry the line number
     CHECK(what_of("a b\nx\n").find("line 2") != std::string::npos);
