@@ -150,7 +150,7 @@ __global__ void hub_split_kernel(const int* __restrict__ deg_sorted, int rows, l
     *hub_counter = 0;
 }
 constexpr int kRowsPerGrab = 2;
-constexpr int kHeavyDegree = 128;  // GGD argmin: rows above this degree use a block each
+constexpr int kHeavyDegree = 256;  // GGD argmin: rows above this degree use a block each
 
 __global__ void row_degree_kernel(const long long* __restrict__ off, int row_begin, int rows, int* __restrict__ deg,
                                   int* __restrict__ id, const int* __restrict__ slab_flags, int b1, int b2, int b3) {
