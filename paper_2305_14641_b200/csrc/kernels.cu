@@ -768,7 +768,7 @@ __global__ void __launch_bounds__(kBlock) successors_class_kernel(const long lon
 // longer serialises on one block. Single-segment rows write their successor
 // directly; longer rows write per-segment partials that a warp per row
 // combines.
-constexpr int kHeavySegment = 512;
+constexpr int kHeavySegment = 1024;
 
 struct HeavyItem {
     int row, seg, slot;  // slot: partial-minimum slot, -1 for single-segment rows
