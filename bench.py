@@ -149,13 +149,14 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sel)}
 
 
-def recorded_traffic(kernel_key, field="dram_bytes"):
-    """A per-launch ncu figure of a kernel from the committed capture
-    (profiles/traffic.json): DRAM bytes by default, or None."""
+def recorded_traffic(workload, kernel_key, field="dram_bytes"):
+    """A per-launch ncu figure of a kernel from the committed capture of THIS
+    workload (profiles/traffic.json, keyed by workload): DRAM bytes by
+    default, or None when that workload has no capture."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
-        return json.load(open(p))[kernel_key][field]
-    except (OSError, KeyError, ValueError):
+        return json.load(open(p))["workloads"][workload][kernel_key][field]
+    except (OSError, KeyError, ValueError, TypeError):
         return None
 
 
@@ -406,6 +407,38 @@ def run_native(args):
                "sample": f"{len(srows)} strided rows x {S} sigmas ({len(srows) * n * S:.3e} pairs) in {el:.1f}s, "
                          f"{what}; GPU rows bit-identical: {same}"}
 
+    # The exact fast-forward moves few bytes per launch; its binding resource
+    # is instruction issue (fp64/int chain arithmetic), so `bound` names that
+    # and `frac` stays the HBM fraction the contract asks for. ncu figures
+    # (traffic, issue) are attached only from a capture of THIS workload.
+    kname = "potential_warp_kernel<FASTFWD,unit>" if args.kernel == "fastfwd" else "potential_warp_kernel<REPLAY,unit>"
+    if args.hop_cap > 1:
+        kname = "k-hop pipeline (khop_expand x2 + segmented sort + khop_walk_kernel)"
+    cap = (lambda f: recorded_traffic(args.workload, kname, f)) if (world == 1 and args.hop_cap == 1) else (
+        lambda f: None)
+    roofline = {
+        "bound": "issue" if args.kernel == "fastfwd" else "fp64",
+        "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
+        "hbm_frac": (achieved / peak) if achieved else None,
+        "traffic": cap("dram_bytes"),
+        "traffic_source": (f"profiles/traffic.json workloads.{args.workload} (ncu --set full, this workload)"
+                           if cap("dram_bytes") is not None else "no ncu capture of this workload"),
+        "kernel": kname, "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
+        "note": ("algorithmic bytes = 8(rows+1) + 4*nnz + 8*rows*S (CSR read once, V written once); the exact "
+                 "fast-forward is issue-bound, so frac is far below 1 by construction: see binding and DESIGN.md"),
+        "binding": ({"resource": "instruction issue" if args.kernel == "fastfwd" else "fp64 pipe",
+                     "issue_slots_busy_pct": cap("issue_active_pct"),
+                     "warp_instructions": cap("inst_executed"),
+                     "active_threads_per_warp": cap("threads_per_warp"),
+                     "fp64_pipe_pct": cap("fp64_pipe_pct"),
+                     "source": f"profiles/traffic.json workloads.{args.workload} (ncu --set full)"}
+                    if cap("inst_executed") is not None else None),
+    }
+
+    e2e_qc = None
+    if rank == 0 and world == 1 and not args.no_e2e and not args.profile and args.hop_cap == 1:
+        e2e_qc = e2e_qc_leg(off, nbr, args.workload)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -424,25 +457,9 @@ def run_native(args):
                                 + ("labels of every sigma on every rank" if args.labels == "replicated" else
                                    "every sigma's labels on the rank owning its sigma chunk, counts on every rank"))},
             "breakdown_ms": dict(breakdown, wall_s_timed_region=wall),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None,
-                         "traffic": (recorded_traffic("potential_warp_kernel<FASTFWD,unit>")
-                                     if world == 1 and args.hop_cap == 1 else None),
-                         "traffic_source": "profiles/traffic.json (ncu --set full, LFR 1M, 32 sigmas)",
-                         "kernel": ("potential_warp_kernel<FASTFWD,unit>" if args.hop_cap == 1 else
-                                    "k-hop pipeline (khop_expand x2 + segmented sort + khop_walk_kernel)"),
-                         "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
-                         "note": "algorithmic bytes = 8(rows+1) + 4*nnz + 8*rows*S; the exact fast-forward is "
-                                 "issue-bound (fp64/int chain arithmetic), see DESIGN.md",
-                         "binding": ({"resource": "instruction issue",
-                                      "issue_slots_busy_pct": recorded_traffic("potential_warp_kernel<FASTFWD,unit>",
-                                                                               "issue_active_pct"),
-                                      "warp_instructions": recorded_traffic("potential_warp_kernel<FASTFWD,unit>",
-                                                                            "inst_executed"),
-                                      "source": "profiles/traffic.json (ncu --set full)"}
-                                     if args.hop_cap == 1 else None)},
+            "roofline": roofline,
             "clocks": clocks, "gpu_launches": gpu_launches,
-            "e2e": e2e, "cpu_baseline": cpu,
+            "e2e": e2e, "cpu_baseline": cpu, "e2e_qc": e2e_qc,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -522,6 +539,45 @@ def e2e_leg(args, N, torch, dist, off, nbr, sig, rank, world, dev, stream, begin
             "d2h_bytes_per_step": int(4 * S * n + 4 * S),
             "api": "gqc_dev_* per rank + NCCL all-to-all(V); each rank downloads its sigma chunk's labels",
             "ms_per_step": t * 1e3}
+
+
+def e2e_qc_leg(off, nbr, workload):
+    """End-to-end QC time, the metric's second half (SURVEY.md §8(d);
+    graphqc_main.cpp:86-157): the `graphqc sweep` CLI on this workload's edge
+    list (text file -> CSR -> 30-sigma default log grid -> GGD -> modularity
+    per sigma -> CSV + mutation line). Two runs in fresh processes; the
+    second is reported (the first pays the page cache), each with the CLI's
+    own stage times."""
+    import re
+    import shutil
+    from bench_tools import graphgen
+    cli = os.path.join(ROOT, "paper_2305_14641_b200", "bin", "graphqc")
+    if not os.path.exists(cli):
+        return {"unavailable": "graphqc CLI not built"}
+    d = tempfile.mkdtemp(prefix="e2e_qc_")
+    try:
+        edges = os.path.join(d, "g.edges")
+        graphgen.write_edge_list(edges, off, nbr)
+        cmd = [cli, "sweep", edges, "--out", os.path.join(d, "sweep.csv")]
+        runs = []
+        for traced in (False, False, True):  # two timed runs, then one with GQC_TRACE stage times
+            env = dict(os.environ)
+            env.pop("GQC_TRACE", None)
+            if traced:
+                env["GQC_TRACE"] = "1"
+            t0 = time.perf_counter()
+            p = subprocess.run(cmd, capture_output=True, text=True, env=env)
+            wall = time.perf_counter() - t0
+            if p.returncode != 0:
+                return {"unavailable": f"graphqc sweep exit {p.returncode}: {p.stderr[-300:]}"}
+            st = {m.group(1): float(m.group(2)) for m in re.finditer(r"\[graphqc\] (\w+)\s+([\d.]+) ms", p.stderr)}
+            runs.append((wall, st, p.stdout.strip().splitlines()[-1:]))
+        return {"seconds": runs[1][0], "first_run_seconds": runs[0][0], "stages_ms": runs[2][1],
+                "stages_source": "a third run with GQC_TRACE=1", "edge_file_bytes": os.path.getsize(edges),
+                "command": "graphqc sweep <edges> --out sweep.csv (default 30-point log grid, modularity per sigma)",
+                "workload": workload, "stdout_tail": runs[1][2]}
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
 
 
 def main():

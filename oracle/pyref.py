@@ -66,6 +66,8 @@ def lib():
                                     P, P]
         L.ref_log_sigma_grid.argtypes = [f64, C.c_int, f64, f64, P]
         L.ref_array_exp.argtypes = [P, i64, f64, P]
+        L.ref_random_graph_seq.restype = P
+        L.ref_random_graph_seq.argtypes = [C.c_uint32, P, i32, f64, f64, i32]
         _lib = L
     return _lib
 
@@ -105,6 +107,17 @@ class Graph:
         nbr = np.ascontiguousarray(nbr, dtype=np.int32)
         wt = None if wt is None else np.ascontiguousarray(wt, dtype=np.float64)
         h = lib().ref_graph_from_csr(len(offsets) - 1, _p(offsets), _p(nbr), _p(wt), W)
+        if not h:
+            raise ValueError(lib().ref_last_error().decode())
+        return cls(h)
+
+    @classmethod
+    def random_seq(cls, seed, ns, avg_degree, W=10.0, unit=False):
+        """The reference's own oracles::random_graph (tests/oracles.hpp:134-154):
+        graphs of ns[0], ns[1], ... nodes drawn in turn from ONE
+        std::mt19937(seed); returns the last one."""
+        ns = np.ascontiguousarray(ns, dtype=np.int32)
+        h = lib().ref_random_graph_seq(seed, _p(ns), len(ns), avg_degree, W, 1 if unit else 0)
         if not h:
             raise ValueError(lib().ref_last_error().decode())
         return cls(h)

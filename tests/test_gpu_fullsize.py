@@ -99,3 +99,53 @@ def test_khop_full_lfr_sampled_rows_and_ggd_properties():
         check_ggd(off, nbr, v[q], succ[q], res[q].center, res[q].cluster_index, res[q].num_clusters)
         ref = O.potentials_khop(off, nbr, None, 10.0, s, 2, workers=16, rows=rows)
         assert np.array_equal(v[q][rows].view(np.int64), ref.view(np.int64)), f"sigma {s}"
+
+
+def _both_kernels(csr, sigmas):
+    """(fast-forward field, dense-replay field), sigma-major [S][N]."""
+    N.set_kernel(N.KERNEL_REPLAY)
+    try:
+        v_replay = N.potentials(csr, sigmas)
+    finally:
+        N.set_kernel(N.KERNEL_FASTFWD)
+    return N.potentials(csr, sigmas), v_replay
+
+
+def test_lfr_full_field_fastfwd_equals_replay_all_sigmas():
+    """The bench's whole field, every row and all 32 sigmas: K2 (exact
+    fast-forward, warp per row) == K1 (dense in-order replay: every one of the
+    N adds of potential.cpp:30-35 performed, ~3.2e13 pairs), bit for bit.
+    K1 is itself pinned to the reference's code on every small graph and on
+    the sampled rows above."""
+    from bench_tools import graphgen
+    from paper_2305_14641_b200.sweep import log_sigma_grid
+    graphgen.build()
+    off, nbr = graphgen.lfr()
+    grid = np.asarray(log_sigma_grid(10.0, 32))
+    v_ff, v_rep = _both_kernels(N.Csr(off, nbr, None, 10.0), grid)
+    for q in range(len(grid)):
+        bad = np.flatnonzero(v_ff[q].view(np.int64) != v_rep[q].view(np.int64))
+        assert bad.size == 0, f"sigma index {q}: {bad.size} rows differ, first {bad[:5]}"
+
+
+def test_rmat_full_field_fastfwd_equals_replay():
+    """R-MAT scale 22 (4.19M nodes, hubs of ~1e5 neighbours): the 32-sigma
+    fast-forward field of the bench (warp per row, batched walk) at grid
+    indices 0, 10, 21 and 31 equals, on every row, the dense replay of those
+    four sigmas through the thread-per-row kernel (~7e13 pairs)."""
+    from bench_tools import graphgen
+    from paper_2305_14641_b200.sweep import log_sigma_grid
+    graphgen.build()
+    off, nbr = graphgen.rmat()
+    grid = np.asarray(log_sigma_grid(10.0, 32))
+    picks = [0, 10, 21, 31]
+    csr = N.Csr(off, nbr, None, 10.0)
+    v_ff = N.potentials(csr, grid)
+    N.set_kernel(N.KERNEL_REPLAY)
+    try:
+        v_rep = N.potentials(csr, grid[picks])
+    finally:
+        N.set_kernel(N.KERNEL_FASTFWD)
+    for k, q in enumerate(picks):
+        bad = np.flatnonzero(v_ff[q].view(np.int64) != v_rep[k].view(np.int64))
+        assert bad.size == 0, f"sigma index {q}: {bad.size} rows differ, first {bad[:5]}"
