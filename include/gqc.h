@@ -21,7 +21,10 @@
  * device and results back; the caller owns every buffer. Errors are status
  * codes mirroring the reference's exception classes; gqc_last_error() returns
  * the message of the calling thread's last failure (same texts as the
- * reference, e.g. "sigma must be positive"). Calls are serialized per process.
+ * reference, e.g. "sigma must be positive"). Each call locks the context of
+ * every device it uses for its whole duration (one lock per device, taken in
+ * ascending device order): calls on different devices, from different host
+ * threads, run concurrently; calls on one device are serialized.
  * There is no CPU fallback: without a usable CUDA device every compute entry
  * point fails with GQC_ECUDA.
  */
@@ -43,7 +46,7 @@ typedef enum gqc_status {
     GQC_EIO = 4,    /* graphqc::IoError */
     GQC_ECUDA = 5,  /* CUDA runtime failure or no device */
     GQC_ENOMEM = 6, /* device or host allocation failure (std::bad_alloc) */
-    GQC_ENCCL = 7   /* reserved for collective failures */
+    GQC_ENCCL = 7   /* collective / peer-memory exchange failures */
 } gqc_status;
 
 /* Undirected CSR exactly as graphqc::Graph stores it (graph.hpp:66-71):
@@ -83,7 +86,17 @@ typedef enum gqc_kernel { GQC_KERNEL_FASTFWD = 0, GQC_KERNEL_REPLAY = 1 } gqc_ke
  * Weighted graphs with K > 1 -> GQC_EINVAL ("k-hop distances need unit
  * weights"). The fast-forward kernel runs either way (GQC_OPT_KERNEL only
  * selects the K = 1 kernel). */
-typedef enum gqc_option { GQC_OPT_EXP_MODE = 1, GQC_OPT_KERNEL = 2, GQC_OPT_DEVICE = 3, GQC_OPT_HOP_CAP = 4 } gqc_option;
+/* GQC_OPT_GPUS (g, default 1): gqc_potentials, gqc_cluster_sweep and
+ * gqc_cluster_sweep_intra run on the g devices GQC_OPT_DEVICE ..
+ * GQC_OPT_DEVICE + g - 1 (see gqc_cluster_sweep_multi); the results are the
+ * same bits for every g. */
+typedef enum gqc_option {
+    GQC_OPT_EXP_MODE = 1,
+    GQC_OPT_KERNEL = 2,
+    GQC_OPT_DEVICE = 3,
+    GQC_OPT_HOP_CAP = 4,
+    GQC_OPT_GPUS = 5
+} gqc_option;
 
 const char* gqc_last_error(void);
 const char* gqc_version(void);
@@ -136,6 +149,36 @@ gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_s
 gqc_status gqc_cluster_sweep_intra(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out,
                                    int32_t* succ_out, int32_t* center_out, int32_t* cluster_index_out,
                                    int32_t* num_clusters_out, int64_t* intra_out);
+
+/* -------------------------------------------------------- multi-device API */
+/* The row-sharded sweep of one process over several GPUs — the reference's
+ * compute_potentials_parallel(g, sigma, workers) (potential.cpp:62-87) with
+ * GPUs as the workers, and its callers cluster (ggd.cpp:59-62) and run_sweep
+ * (sweep.cpp:50-57) for a whole sigma grid.
+ *
+ * devices[r] is the CUDA device of shard r (0 <= r < n_shards <= 32; a device
+ * may be listed more than once and then hosts several shards). Shard r
+ * computes the potentials of the row block gqc_row_shards() assigns it for
+ * every sigma and owns sigma chunk r (ceil(n_sigma / n_shards) sigmas): its
+ * potential kernel stores each chunk of its rows directly into the owning
+ * shard's field over peer memory (NVLink/NVSwitch; staged + peer copy when
+ * two devices cannot access each other), then every shard runs GGD for its
+ * own chunk and writes its labels to the caller's sigma-major outputs. The
+ * whole CSR is uploaded to every device. Outputs and errors are exactly those
+ * of gqc_cluster_sweep_intra / gqc_potentials, bit for bit, for any shard
+ * count. n_shards == 1 runs the single-device pipeline on devices[0]. */
+gqc_status gqc_cluster_sweep_multi(const gqc_csr* g, const double* sigmas, int32_t n_sigma, const int32_t* devices,
+                                   int32_t n_shards, double* v_out, int32_t* succ_out, int32_t* center_out,
+                                   int32_t* cluster_index_out, int32_t* num_clusters_out, int64_t* intra_out);
+gqc_status gqc_potentials_multi(const gqc_csr* g, const double* sigmas, int32_t n_sigma, const int32_t* devices,
+                                int32_t n_shards, double* v_out);
+
+/* Row blocks of a multi-device sweep: bounds[0] = 0 <= bounds[1] <= ... <=
+ * bounds[n_shards] = n, shard r = rows [bounds[r], bounds[r+1]). Balanced by
+ * the fast-forward kernel's cost per row (~ degree + 16), i.e. by an nnz
+ * prefix over offsets; equal blocks w*floor(n/k) + min(w, n mod k)
+ * (potential.cpp:70-74) under GQC_KERNEL_REPLAY, whose rows all cost n. */
+gqc_status gqc_row_shards(const gqc_csr* g, int32_t n_shards, int32_t* bounds);
 
 /* -------------------------------------------------------------- device API */
 /* All pointers in gqc_csr and the buffers below are device pointers on the

@@ -6,11 +6,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <string>
@@ -26,14 +28,36 @@ namespace {
 
 thread_local std::string t_err;
 thread_local long long t_launches = 0;
-std::mutex g_mu;  // calls are serialized per process
 
+// Options: process-wide, set by gqc_set_option; every call works on a
+// snapshot taken when it starts (t_opt), so a concurrent set never changes a
+// call halfway.
 struct Options {
     int exp_mode = GQC_EXP_EIGEN;
     int kernel = GQC_KERNEL_FASTFWD;
-    int device = 0;  // device of the host-buffer entry points (GQC_OPT_DEVICE)
+    int device = 0;   // device of the host-buffer entry points (GQC_OPT_DEVICE)
     int hop_cap = 1;  // distance model (GQC_OPT_HOP_CAP): 1 = the reference's
+    int gpus = 1;     // devices of the host-buffer sweep entry points (GQC_OPT_GPUS)
+};
+struct AtomicOptions {
+    std::atomic<int> exp_mode{GQC_EXP_EIGEN}, kernel{GQC_KERNEL_FASTFWD}, device{0}, hop_cap{1}, gpus{1};
+    Options load() const {
+        Options o;
+        o.exp_mode = exp_mode.load();
+        o.kernel = kernel.load();
+        o.device = device.load();
+        o.hop_cap = hop_cap.load();
+        o.gpus = gpus.load();
+        return o;
+    }
 } g_opt;
+thread_local Options t_opt;
+
+// Locking: one mutex per device context instead of one per process. A call
+// locks the context of every device it touches for its whole duration (a
+// multi-device call locks its devices in ascending order), so calls on
+// different devices, from different host threads, run concurrently.
+thread_local std::vector<std::mutex*> t_held;
 
 struct Fail {
     gqc_status st;
@@ -49,10 +73,18 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 void cuda_check(int e, const char* what) { cuda_check(static_cast<cudaError_t>(e), what); }
 
+struct HeldLocks {  // releases the device locks a call took, in reverse order
+    ~HeldLocks() {
+        for (auto it = t_held.rbegin(); it != t_held.rend(); ++it) (*it)->unlock();
+        t_held.clear();
+    }
+};
+
 template <class F>
 gqc_status guarded(F&& f) {
-    std::lock_guard<std::mutex> lock(g_mu);
     t_launches = 0;
+    t_opt = g_opt.load();
+    HeldLocks release;
     try {
         f();
         return GQC_OK;
@@ -118,18 +150,41 @@ struct DevBuf {
     }
 };
 
+// Scratch tables of a potential launch on weighted graphs (host-evaluated
+// exp values the device reads): one set per context and per multi-device shard.
+struct PotScratch {
+    DevBuf tail, entry;
+};
+
+// Buffers and stream of one shard of a multi-device sweep (gqc_*_multi):
+// its sigma chunk's node-major field (written by every shard's potential
+// kernel over peer memory), the chunk's GGD outputs and a staging area for
+// devices without peer access. Owned by the shard's device context.
+struct ShardBufs {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev_pot = nullptr;
+    DevBuf v, v_sm, succ, center, ci, nc, ws, intra, send;
+    PotScratch scr;
+    int* nc_host = nullptr;  // pinned counts staging
+    int nc_host_cap = 0;
+};
+
 struct DeviceCtx {
+    std::mutex mu;  // held for the whole duration of a call on this device
+    int dev = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t copy = nullptr;   // host<->device copies overlapped with compute
     cudaStream_t slab[4] = {};     // concurrent per-slab potential launches
     cudaEvent_t ev[16] = {};
     cudaEvent_t slab_done[4] = {};
     cudaMemPool_t pool = nullptr;  // stream-ordered scratch that keeps its memory
-    DevBuf off, nbr, w, v_nm, v_sm, succ, center, ci, nc, ws, tail, entry, intra;
+    DevBuf off, nbr, w, v_nm, v_sm, succ, center, ci, nc, ws, intra;
+    PotScratch scr;
     int* nc_host = nullptr;  // pinned staging for per-sigma counts (cudaHostAlloc)
     int nc_host_cap = 0;
     DevBuf slab_sync;            // polled upload: [4] slab flags, [4] error word
     int* slab_host = nullptr;    // pinned: [0..3] = 1 (flag sources), [4] error readback
+    std::vector<std::unique_ptr<ShardBufs>> shards;  // multi-device shards on this device
 };
 
 // Device->host copies into pageable memory block the calling thread until
@@ -143,17 +198,18 @@ bool host_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
-int* pinned_counts(DeviceCtx& C, int n) {
-    if (C.nc_host_cap < n) {
-        if (C.nc_host) cudaFreeHost(C.nc_host);
-        C.nc_host = nullptr;
-        C.nc_host_cap = 0;
-        cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&C.nc_host), sizeof(int) * n, cudaHostAllocDefault),
+int* pinned_counts_buf(int*& buf, int& cap, int n) {
+    if (cap < n) {
+        if (buf) cudaFreeHost(buf);
+        buf = nullptr;
+        cap = 0;
+        cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&buf), sizeof(int) * n, cudaHostAllocDefault),
                    "cudaHostAlloc");
-        C.nc_host_cap = n;
+        cap = n;
     }
-    return C.nc_host;
+    return buf;
 }
+int* pinned_counts(DeviceCtx& C, int n) { return pinned_counts_buf(C.nc_host, C.nc_host_cap, n); }
 
 // libgqc carries its own (static) CUDA runtime, whose current device is not
 // the caller's (torch.cuda.set_device does not reach it). Every call binds it
@@ -161,7 +217,7 @@ int* pinned_counts(DeviceCtx& C, int n) {
 // stream (or of a buffer when the stream is the legacy default), host-buffer
 // entry points to GQC_OPT_DEVICE.
 void bind_device(cudaStream_t st, const void* dptr) {
-    int dev = g_opt.device;
+    int dev = t_opt.device;
     if (st) {
         cuda_check(cudaStreamGetDevice(st, &dev), "cudaStreamGetDevice");
     } else if (dptr) {
@@ -172,17 +228,32 @@ void bind_device(cudaStream_t st, const void* dptr) {
     cuda_check(cudaSetDevice(dev), "cudaSetDevice");
 }
 
-DeviceCtx& ctx(cudaStream_t st = nullptr, const void* dptr = nullptr) {  // callers hold g_mu (guarded)
-    static std::map<int, DeviceCtx> all;
-    int dev = 0;
+int visible_devices() {
     int count = 0;
-    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    if (cudaGetDeviceCount(&count) != cudaSuccess) {
         cudaGetLastError();
-        fail(GQC_ECUDA, "no CUDA device available (libgqc has no CPU path)");
+        count = 0;
     }
-    bind_device(st, dptr);
-    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-    DeviceCtx& c = all[dev];
+    return count;
+}
+
+// The context of device `dev`, locked by this call (see t_held) and created
+// on first use; the calling thread is bound to the device.
+DeviceCtx& ctx_of(int dev) {
+    static std::mutex map_mu;
+    static std::map<int, DeviceCtx> all;
+    DeviceCtx* cp;
+    {
+        std::lock_guard<std::mutex> l(map_mu);
+        cp = &all[dev];
+    }
+    DeviceCtx& c = *cp;
+    if (std::find(t_held.begin(), t_held.end(), &c.mu) == t_held.end()) {
+        c.mu.lock();
+        t_held.push_back(&c.mu);
+    }
+    c.dev = dev;
+    cuda_check(cudaSetDevice(dev), "cudaSetDevice");
     if (!c.stream) {
         cuda_check(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking), "cudaStreamCreate");
         cuda_check(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -200,6 +271,25 @@ DeviceCtx& ctx(cudaStream_t st = nullptr, const void* dptr = nullptr) {  // call
         cuda_check(cudaMemPoolSetAttribute(c.pool, cudaMemPoolAttrReleaseThreshold, &keep), "cudaMemPoolSetAttribute");
     }
     return c;
+}
+
+DeviceCtx& ctx(cudaStream_t st = nullptr, const void* dptr = nullptr) {
+    if (visible_devices() == 0) fail(GQC_ECUDA, "no CUDA device available (libgqc has no CPU path)");
+    bind_device(st, dptr);
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    return ctx_of(dev);
+}
+
+ShardBufs& shard_bufs(DeviceCtx& C, std::size_t slot) {
+    while (C.shards.size() <= slot) C.shards.emplace_back(new ShardBufs);
+    ShardBufs& B = *C.shards[slot];
+    if (!B.stream) {
+        cuda_check(cudaSetDevice(C.dev), "cudaSetDevice");
+        cuda_check(cudaStreamCreateWithFlags(&B.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        cuda_check(cudaEventCreateWithFlags(&B.ev_pot, cudaEventDisableTiming), "cudaEventCreate");
+    }
+    return B;
 }
 
 void check_csr_shape(const gqc_csr* g) {
@@ -247,14 +337,20 @@ struct SlabSync {  // polled CSR upload (see PotentialLaunch::slab_flags)
     int* err = nullptr;
 };
 
+// peer (optional): per sigma chunk q of out_chunk sigmas, where row
+// row_begin's slot of that chunk lives (node-major rows of out_chunk values,
+// on any device this one can address): the multi-device sweep's fused
+// exchange. scr: scratch for weighted tables (default: the context's).
 void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S, int row_begin, int row_end,
                     double* v_nm, const double* host_w, cudaStream_t st, const std::int64_t* host_off = nullptr,
-                    int out_chunk = 0, long long out_chunk_stride = 0, const SlabSync* sync = nullptr) {
+                    int out_chunk = 0, long long out_chunk_stride = 0, const SlabSync* sync = nullptr,
+                    double* const* peer = nullptr, PotScratch* scr = nullptr) {
+    if (!scr) scr = &C.scr;
     const int n = g.n;
-    const int mode = g_opt.exp_mode;
+    const int mode = t_opt.exp_mode;
     const bool weighted = g.w != nullptr;
     const bool tail = (mode == GQC_EXP_EIGEN) && (n % 2 == 1);
-    const int K = g_opt.hop_cap;
+    const int K = t_opt.hop_cap;
     if (K > 1 && weighted) fail(GQC_EINVAL, "k-hop distances need unit weights");
     if (K > 1 && n >= (1 << 29)) fail(GQC_EINVAL, "k-hop distances need fewer than 2^29 nodes");
 
@@ -315,6 +411,11 @@ void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S,
         P.out_chunk = out_chunk > 0 ? out_chunk : S;  // packed sigma chunks, or plain rows of S
         P.out_ld = P.out_chunk;
         P.out_chunk_stride = out_chunk > 0 ? out_chunk_stride : 0;
+        if (peer) {
+            P.out_peer = 1;
+            const int chunks = (S + P.out_chunk - 1) / P.out_chunk;
+            for (int q = 0; q < chunks && q < kMaxShards; ++q) P.out_chunk_ptr[q] = peer[q];
+        }
         if (sync) {
             P.slab_flags = sync->flags;
             for (int k = 0; k < 5; ++k) P.slab_bound[k] = sync->bound[k];
@@ -340,7 +441,7 @@ void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S,
                 std::vector<double> d2(last_deg), tab(last_deg * Sc);
                 for (long long q = 0; q < last_deg; ++q) d2[q] = last_w[q] * last_w[q];
                 host_exp_table(d2.data(), last_deg, neg_inv, Sc, tab.data());
-                double* dtab = C.tail.get<double>(tab.size());
+                double* dtab = scr->tail.get<double>(tab.size());
                 cuda_check(cudaMemcpyAsync(dtab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, st),
                            "copy tail table");
                 cuda_check(cudaStreamSynchronize(st), "sync");  // tab is a local
@@ -350,7 +451,7 @@ void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S,
             P.weight_mode = kEntryTable;
             std::vector<double> tab(static_cast<std::size_t>(g.nnz) * Sc);
             host_exp_table(all_d2.data(), g.nnz, neg_inv, Sc, tab.data());
-            double* dtab = C.entry.get<double>(std::max<std::size_t>(tab.size(), 1));
+            double* dtab = scr->entry.get<double>(std::max<std::size_t>(tab.size(), 1));
             if (!tab.empty())
                 cuda_check(cudaMemcpyAsync(dtab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice, st),
                            "copy entry table");
@@ -359,7 +460,7 @@ void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S,
             P.entry_ld = Sc;
             P.entry_col0 = 0;
         }
-        cuda_check(launch_potentials(P, g_opt.kernel, C.pool, st), "potential kernel launch");
+        cuda_check(launch_potentials(P, t_opt.kernel, C.pool, st), "potential kernel launch");
     }
 }
 
@@ -427,7 +528,7 @@ bool class_order_enabled() {
 void make_class_order(DeviceCtx& C, const gqc_csr& g, const double* v, int ld, int S, cudaStream_t st,
                       ClassOrderScope& out) {
     // weighted graphs and k-hop fields are not degree-determined: plain argmin
-    if (!class_order_enabled() || g.w || g_opt.hop_cap > 1) return;
+    if (!class_order_enabled() || g.w || t_opt.hop_cap > 1) return;
     const int n = g.n;
     const std::int64_t* off = g.offsets;
     const long long nnz = g.nnz;
@@ -437,6 +538,19 @@ void make_class_order(DeviceCtx& C, const gqc_csr& g, const double* v, int ld, i
 }  // namespace
 
 void count_launch(int k) { t_launches += k; }
+
+int sm_count() {
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    int v = cache[dev].load();
+    if (!v) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev].store(v);
+    }
+    return v;
+}
 
 }  // namespace gqc
 
@@ -460,6 +574,10 @@ int32_t gqc_device_count(void) {
 static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out,
                                int32_t* succ_out, int32_t* center_out, int32_t* cluster_index_out,
                                int32_t* num_clusters_out, int64_t* intra_out = nullptr);
+static void sweep_multi_impl(const gqc_csr* g, const double* sigmas, int S, const int* devices, int shards,
+                             double* v_out, int* succ_out, int* center_out, int* ci_out, int* nc_out,
+                             std::int64_t* intra_out, bool potentials_only);
+static std::vector<int> option_devices();
 
 gqc_status gqc_init(void) {
     return guarded([&] {
@@ -489,13 +607,11 @@ gqc_status gqc_set_option(gqc_option key, int64_t value) {
             if (value < 1 || value > kMaxHopCap) fail(GQC_EINVAL, "hop cap must be in 1..7");
             g_opt.hop_cap = static_cast<int>(value);
         } else if (key == GQC_OPT_DEVICE) {
-            int count = 0;
-            if (cudaGetDeviceCount(&count) != cudaSuccess) {
-                cudaGetLastError();
-                count = 0;
-            }
-            if (value < 0 || value >= count) fail(GQC_EINVAL, "device ordinal out of range");
+            if (value < 0 || value >= visible_devices()) fail(GQC_EINVAL, "device ordinal out of range");
             g_opt.device = static_cast<int>(value);
+        } else if (key == GQC_OPT_GPUS) {
+            if (value < 1 || value > kMaxShards) fail(GQC_EINVAL, "gpu count must be in 1..32");
+            g_opt.gpus = static_cast<int>(value);
         } else {
             fail(GQC_EINVAL, "unknown option");
         }
@@ -509,12 +625,19 @@ gqc_status gqc_get_option(gqc_option key, int64_t* value) {
         else if (key == GQC_OPT_KERNEL) *value = g_opt.kernel;
         else if (key == GQC_OPT_DEVICE) *value = g_opt.device;
         else if (key == GQC_OPT_HOP_CAP) *value = g_opt.hop_cap;
+        else if (key == GQC_OPT_GPUS) *value = g_opt.gpus;
         else fail(GQC_EINVAL, "unknown option");
     });
 }
 
 gqc_status gqc_potentials(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out) {
     return guarded([&] {
+        if (t_opt.gpus > 1) {
+            const std::vector<int> d = option_devices();
+            sweep_multi_impl(g, sigmas, n_sigma, d.data(), static_cast<int>(d.size()), v_out, nullptr, nullptr, nullptr,
+                             nullptr, nullptr, true);
+            return;
+        }
         check_sigmas(sigmas, n_sigma);
         check_csr_shape(g);
         if (!v_out) fail(GQC_EINVAL, "null output");
@@ -603,7 +726,7 @@ gqc_status gqc_resolve_centers(int32_t n, const int32_t* succ, int32_t* center, 
 // the next pass computes, so the last pass's download is the exposed tail
 constexpr int kGgdChunk = GQC_GGD_CHUNK;
 
-// The body of gqc_cluster_sweep (callers hold g_mu).
+// The body of gqc_cluster_sweep (inside guarded()).
 static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out, int32_t* succ_out,
                         int32_t* center_out, int32_t* cluster_index_out, int32_t* num_clusters_out,
                         int64_t* intra_out) {
@@ -618,7 +741,7 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
         const int n = g->n;
         const long long nnz = g->nnz;
         const bool weighted = g->w && !all_unit(g->w, nnz);
-        if (g_opt.hop_cap > 1 && weighted) fail(GQC_EINVAL, "k-hop distances need unit weights");
+        if (t_opt.hop_cap > 1 && weighted) fail(GQC_EINVAL, "k-hop distances need unit weights");
         if (intra_out && weighted) fail(GQC_EINVAL, "intra counts need unit weights");
 
         // Pipeline: the CSR goes up in row slabs on the copy stream while the
@@ -645,7 +768,7 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
             }
         }
         // (k-hop rows read their neighbours' rows too: one slab, the whole CSR)
-        const int slabs = (nnz >= (1 << 20) && g_opt.hop_cap == 1) ? 4 : 1;
+        const int slabs = (nnz >= (1 << 20) && t_opt.hop_cap == 1) ? 4 : 1;
         const bool polled = slabs == 4 && !weighted && n_sigma >= 8 && polled_upload_enabled();
         std::vector<int> bound(slabs + 1, n);
         bound[0] = 0;
@@ -806,20 +929,291 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
     }
 }
 
+// ------------------------------------------------------------ multi-device
+// Row shards of a multi-device sweep (gqc_row_shards): contiguous row blocks
+// balanced by the fast-forward kernel's cost, ~ deg(i) + kRowCost per row.
+// The reference's equal blocks (potential.cpp:70-74) balance its O(N) rows
+// only; they are kept for the dense replay, whose rows all cost N.
+constexpr long long kRowCost = 16;
+
+static std::vector<int> row_shards(const std::int64_t* off, int n, int shards, int kernel) {
+    std::vector<int> b(shards + 1, n);
+    b[0] = 0;
+    const long long total = off[n] + kRowCost * n;
+    for (int r = 1; r < shards; ++r) {
+        if (kernel == GQC_KERNEL_REPLAY) {  // potential.cpp:70-74
+            b[r] = static_cast<int>(static_cast<long long>(n / shards) * r + std::min(r, n % shards));
+            continue;
+        }
+        const long long target = total / shards * r + (total % shards) * r / shards;
+        int lo = b[r - 1], hi = n;  // first row i with off[i] + kRowCost * i >= target
+        while (lo < hi) {
+            const int mid = lo + (hi - lo) / 2;
+            if (off[mid] + kRowCost * mid < target) lo = mid + 1;
+            else hi = mid;
+        }
+        b[r] = lo;
+    }
+    return b;
+}
+
+// The sweep over `shards` shards on devices[0..shards) (repeats allowed: a
+// device then hosts several shards). Shard r computes the potentials of rows
+// [rb[r], rb[r+1]) for every sigma; the potential kernel writes sigma chunk
+// q (chunk = ceil(S / shards) sigmas) of those rows straight into shard q's
+// node-major field V_q[n][chunk] on shard q's device (peer stores over
+// NVLink: the kernel IS the exchange; without peer access the chunk is
+// staged locally and copied peer-to-peer). Once every shard's potentials are
+// done (cross-device event waits), shard q runs GGD for its sigma chunk and
+// its labels go straight to the caller's sigma-major output. Bit-identical
+// to the single-device sweep for any shard count: rows and sigmas are
+// independent (potential.cpp:18-37, ggd.cpp:7-57).
+static void sweep_multi_impl(const gqc_csr* g, const double* sigmas, int S, const int* devices, int shards, double* v_out,
+                      int* succ_out, int* center_out, int* ci_out, int* nc_out, std::int64_t* intra_out,
+                      bool potentials_only) {
+    check_sigmas(sigmas, S);
+    check_csr_shape(g);
+    if (shards < 1 || shards > kMaxShards) fail(GQC_EINVAL, "shard count must be in 1..32");
+    if (!devices) fail(GQC_EINVAL, "null device list");
+    const int count = visible_devices();
+    if (count == 0) fail(GQC_ECUDA, "no CUDA device available (libgqc has no CPU path)");
+    for (int r = 0; r < shards; ++r)
+        if (devices[r] < 0 || devices[r] >= count) fail(GQC_EINVAL, "device ordinal out of range");
+    if (potentials_only ? !v_out : (!ci_out || !nc_out)) fail(GQC_EINVAL, "null output");
+    if (g->offsets[0] != 0 || g->offsets[g->n] != g->nnz) fail(GQC_EINVAL, "CSR offsets do not match nnz");
+    const int n = g->n;
+    const long long nnz = g->nnz;
+    const bool weighted = g->w && !all_unit(g->w, nnz);
+    if (t_opt.hop_cap > 1 && weighted) fail(GQC_EINVAL, "k-hop distances need unit weights");
+    if (intra_out && weighted) fail(GQC_EINVAL, "intra counts need unit weights");
+
+    // devices locked in ascending order: concurrent multi-device calls cannot deadlock
+    std::vector<int> uniq(devices, devices + shards);
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    std::map<int, DeviceCtx*> C;
+    for (int d : uniq) C[d] = &ctx_of(d);
+    std::map<std::pair<int, int>, bool> direct;  // (writer, owner): peer stores possible
+    for (int a : uniq)
+        for (int b : uniq) {
+            if (a == b) continue;
+            int can = 0;
+            if (cudaDeviceCanAccessPeer(&can, a, b) != cudaSuccess) can = 0;
+            if (can) {
+                cuda_check(cudaSetDevice(a), "cudaSetDevice");
+                cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) e = cudaSuccess;
+                if (e != cudaSuccess) can = 0;
+                cudaGetLastError();
+            }
+            direct[{a, b}] = can != 0;
+        }
+
+    // the CSR on every device (its copy stream); potentials wait on it
+    std::map<int, gqc_csr> dcsr;
+    for (int d : uniq) {
+        DeviceCtx& X = *C[d];
+        cuda_check(cudaSetDevice(d), "cudaSetDevice");
+        gqc_csr dg = *g;
+        auto* off = X.off.get<std::int64_t>(n + 1);
+        auto* nbr = X.nbr.get<std::int32_t>(std::max<long long>(nnz, 1));
+        cuda_check(cudaMemcpyAsync(off, g->offsets, (n + 1) * sizeof(std::int64_t), cudaMemcpyHostToDevice, X.copy),
+                   "copy offsets");
+        if (nnz)
+            cuda_check(cudaMemcpyAsync(nbr, g->nbr, nnz * sizeof(std::int32_t), cudaMemcpyHostToDevice, X.copy),
+                       "copy nbr");
+        dg.offsets = off;
+        dg.nbr = nbr;
+        dg.w = nullptr;
+        if (weighted) {
+            auto* w = X.w.get<double>(std::max<long long>(nnz, 1));
+            cuda_check(cudaMemcpyAsync(w, g->w, nnz * sizeof(double), cudaMemcpyHostToDevice, X.copy), "copy weights");
+            dg.w = w;
+        }
+        cuda_check(cudaEventRecord(X.ev[0], X.copy), "event");
+        dcsr[d] = dg;
+    }
+
+    const std::vector<int> rb = row_shards(g->offsets, n, shards, t_opt.kernel);
+    const int chunk = (S + shards - 1) / shards;
+    const int nchunks = (S + chunk - 1) / chunk;
+    auto s_begin = [&](int q) { return std::min(S, q * chunk); };
+    auto s_count = [&](int q) { return std::min(S, (q + 1) * chunk) - s_begin(q); };
+    std::vector<ShardBufs*> B(shards);
+    {
+        std::map<int, std::size_t> slot;
+        for (int r = 0; r < shards; ++r) B[r] = &shard_bufs(*C[devices[r]], slot[devices[r]]++);
+    }
+    std::vector<double*> V(shards, nullptr);
+    for (int q = 0; q < nchunks; ++q) {
+        cuda_check(cudaSetDevice(devices[q]), "cudaSetDevice");
+        V[q] = B[q]->v.get<double>(static_cast<std::size_t>(n) * chunk);
+    }
+
+    // potentials: shard r's rows for every sigma, each chunk into its owner's V
+    for (int r = 0; r < shards; ++r) {
+        const int d = devices[r];
+        DeviceCtx& X = *C[d];
+        cuda_check(cudaSetDevice(d), "cudaSetDevice");
+        cudaStream_t st = B[r]->stream;
+        cuda_check(cudaStreamWaitEvent(st, X.ev[0], 0), "wait");
+        const int rows = rb[r + 1] - rb[r];
+        double* ptr[kMaxShards] = {};
+        std::vector<int> staged;
+        for (int q = 0; q < nchunks; ++q) {
+            if (devices[q] == d || direct[{d, devices[q]}]) ptr[q] = V[q] + static_cast<std::size_t>(rb[r]) * chunk;
+            else staged.push_back(q);
+        }
+        if (!staged.empty()) {
+            double* send = B[r]->send.get<double>(std::max<std::size_t>(1, static_cast<std::size_t>(rows) * chunk * nchunks));
+            for (int q : staged) ptr[q] = send + static_cast<std::size_t>(q) * rows * chunk;
+        }
+        if (rows > 0) {
+            run_potentials(X, dcsr[d], sigmas, S, rb[r], rb[r + 1], nullptr, weighted ? g->w : nullptr, st, g->offsets,
+                           chunk, 0, nullptr, ptr, &B[r]->scr);
+            for (int q : staged)
+                cuda_check(cudaMemcpyPeerAsync(V[q] + static_cast<std::size_t>(rb[r]) * chunk, devices[q], ptr[q], d,
+                                               static_cast<std::size_t>(rows) * chunk * sizeof(double), st),
+                           "peer copy");
+        }
+        cuda_check(cudaEventRecord(B[r]->ev_pot, st), "event");
+    }
+
+    // GGD of every sigma chunk on its owner once all potentials are in
+    for (int q = 0; q < nchunks; ++q) {
+        const int d = devices[q], Sq = s_count(q), s0 = s_begin(q);
+        DeviceCtx& X = *C[d];
+        ShardBufs& Bq = *B[q];
+        cuda_check(cudaSetDevice(d), "cudaSetDevice");
+        cudaStream_t st = Bq.stream;
+        for (int r = 0; r < shards; ++r)
+            if (r != q) cuda_check(cudaStreamWaitEvent(st, B[r]->ev_pot, 0), "wait");
+        const std::size_t cells = static_cast<std::size_t>(Sq) * n;
+        if (v_out) {
+            double* vsm = Bq.v_sm.get<double>(static_cast<std::size_t>(chunk) * n);
+            cuda_check(launch_transpose(V[q], n, chunk, vsm, st), "transpose");
+        }
+        if (potentials_only) continue;
+        const gqc_csr& dg = dcsr[d];
+        int* ds = Bq.succ.get<int>(cells);
+        int* dc = Bq.center.get<int>(cells);
+        int* dci = Bq.ci.get<int>(cells);
+        int* dnc = Bq.nc.get<int>(Sq);
+        const std::size_t wsb = labels_workspace_bytes(n, Sq);
+        void* ws = Bq.ws.get<char>(wsb);
+        ClassOrderScope order;
+        make_class_order(X, dg, V[q], chunk, Sq, st, order);
+        cuda_check(launch_successors(n, dg.offsets, dg.nbr, V[q], chunk, 0, Sq, 0, n, ds, 1, n, nnz, X.pool, st,
+                                     order.get()),
+                   "successor kernel");
+        cuda_check(launch_chase(n, Sq, ds, dc, st, ws), "chase kernel");
+        cuda_check(launch_labels(n, Sq, dc, dci, dnc, ws, wsb, st, true), "label kernels");
+        if (intra_out)
+            cuda_check(launch_intra_counts(n, Sq, dg.offsets, dg.nbr, dci, Bq.intra.get<long long>(Sq), st),
+                       "intra counts");
+        (void)s0;
+    }
+    // downloads (queued after every launch: a pageable copy blocks the host)
+    for (int q = 0; q < nchunks; ++q) {
+        const int d = devices[q], Sq = s_count(q), s0 = s_begin(q);
+        ShardBufs& Bq = *B[q];
+        cuda_check(cudaSetDevice(d), "cudaSetDevice");
+        cudaStream_t st = Bq.stream;
+        const std::size_t o = static_cast<std::size_t>(s0) * n, cells = static_cast<std::size_t>(Sq) * n;
+        if (v_out)
+            cuda_check(cudaMemcpyAsync(v_out + o, Bq.v_sm.get<double>(static_cast<std::size_t>(chunk) * n),
+                                       cells * sizeof(double), cudaMemcpyDeviceToHost, st),
+                       "copy V");
+        if (potentials_only) continue;
+        if (succ_out)
+            cuda_check(cudaMemcpyAsync(succ_out + o, Bq.succ.get<int>(cells), cells * sizeof(int), cudaMemcpyDeviceToHost, st),
+                       "copy succ");
+        if (center_out)
+            cuda_check(cudaMemcpyAsync(center_out + o, Bq.center.get<int>(cells), cells * sizeof(int),
+                                       cudaMemcpyDeviceToHost, st),
+                       "copy center");
+        cuda_check(cudaMemcpyAsync(ci_out + o, Bq.ci.get<int>(cells), cells * sizeof(int), cudaMemcpyDeviceToHost, st),
+                   "copy cluster index");
+        int* stage = pinned_counts_buf(Bq.nc_host, Bq.nc_host_cap, Sq);
+        cuda_check(cudaMemcpyAsync(stage, Bq.nc.get<int>(Sq), Sq * sizeof(int), cudaMemcpyDeviceToHost, st),
+                   "copy counts");
+        if (intra_out)
+            cuda_check(cudaMemcpyAsync(intra_out + s0, Bq.intra.get<long long>(Sq), Sq * sizeof(long long),
+                                       cudaMemcpyDeviceToHost, st),
+                       "copy intra counts");
+    }
+    for (int r = 0; r < shards; ++r) {
+        cuda_check(cudaSetDevice(devices[r]), "cudaSetDevice");
+        cuda_check(cudaStreamSynchronize(B[r]->stream), "multi-device sweep");
+    }
+    if (!potentials_only)
+        for (int q = 0; q < nchunks; ++q) std::copy(B[q]->nc_host, B[q]->nc_host + s_count(q), nc_out + s_begin(q));
+}
+
+// Devices of the host-buffer entry points: GQC_OPT_DEVICE .. + GQC_OPT_GPUS - 1.
+static std::vector<int> option_devices() {
+    std::vector<int> d(t_opt.gpus);
+    const int count = visible_devices();
+    for (int k = 0; k < t_opt.gpus; ++k) {
+        d[k] = t_opt.device + k;
+        if (d[k] >= count) fail(GQC_EINVAL, "GQC_OPT_GPUS exceeds the visible devices");
+    }
+    return d;
+}
+
 gqc_status gqc_cluster_sweep(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out,
                              int32_t* succ_out, int32_t* center_out, int32_t* cluster_index_out,
                              int32_t* num_clusters_out) {
-    return guarded([&] {
-        cluster_sweep_impl(g, sigmas, n_sigma, v_out, succ_out, center_out, cluster_index_out, num_clusters_out);
-    });
+    return gqc_cluster_sweep_intra(g, sigmas, n_sigma, v_out, succ_out, center_out, cluster_index_out,
+                                   num_clusters_out, nullptr);
 }
 
 gqc_status gqc_cluster_sweep_intra(const gqc_csr* g, const double* sigmas, int32_t n_sigma, double* v_out,
                                    int32_t* succ_out, int32_t* center_out, int32_t* cluster_index_out,
                                    int32_t* num_clusters_out, int64_t* intra_out) {
     return guarded([&] {
+        if (t_opt.gpus > 1) {
+            const std::vector<int> d = option_devices();
+            sweep_multi_impl(g, sigmas, n_sigma, d.data(), static_cast<int>(d.size()), v_out, succ_out, center_out,
+                             cluster_index_out, num_clusters_out, intra_out, false);
+            return;
+        }
         cluster_sweep_impl(g, sigmas, n_sigma, v_out, succ_out, center_out, cluster_index_out, num_clusters_out,
                            intra_out);
+    });
+}
+
+gqc_status gqc_cluster_sweep_multi(const gqc_csr* g, const double* sigmas, int32_t n_sigma, const int32_t* devices,
+                                   int32_t n_shards, double* v_out, int32_t* succ_out, int32_t* center_out,
+                                   int32_t* cluster_index_out, int32_t* num_clusters_out, int64_t* intra_out) {
+    return guarded([&] {
+        if (n_shards == 1 && devices) {  // one shard: the single-device pipeline on that device
+            if (devices[0] < 0 || devices[0] >= visible_devices()) fail(GQC_EINVAL, "device ordinal out of range");
+            t_opt.device = devices[0];
+            cluster_sweep_impl(g, sigmas, n_sigma, v_out, succ_out, center_out, cluster_index_out, num_clusters_out,
+                               intra_out);
+            return;
+        }
+        sweep_multi_impl(g, sigmas, n_sigma, devices, n_shards, v_out, succ_out, center_out, cluster_index_out,
+                         num_clusters_out, intra_out, false);
+    });
+}
+
+gqc_status gqc_potentials_multi(const gqc_csr* g, const double* sigmas, int32_t n_sigma, const int32_t* devices,
+                                int32_t n_shards, double* v_out) {
+    return guarded([&] {
+        sweep_multi_impl(g, sigmas, n_sigma, devices, n_shards, v_out, nullptr, nullptr, nullptr, nullptr, nullptr, true);
+    });
+}
+
+gqc_status gqc_row_shards(const gqc_csr* g, int32_t n_shards, int32_t* bounds) {
+    return guarded([&] {
+        check_csr_shape(g);
+        if (n_shards < 1 || n_shards > kMaxShards) fail(GQC_EINVAL, "shard count must be in 1..32");
+        if (!bounds) fail(GQC_EINVAL, "null output");
+        if (g->offsets[0] != 0 || g->offsets[g->n] != g->nnz) fail(GQC_EINVAL, "CSR offsets do not match nnz");
+        const std::vector<int> b = row_shards(g->offsets, g->n, n_shards, t_opt.kernel);
+        std::copy(b.begin(), b.end(), bounds);
     });
 }
 

@@ -18,6 +18,7 @@ struct SigmaConsts {
 };
 constexpr int kSigmaFields = 10;
 constexpr int kMaxSigmaPerLaunch = 32;
+constexpr int kMaxShards = 32;  // shards of a multi-device sweep (one sigma chunk each)
 
 double host_pexp(double x);
 double host_glibc_exp(double x);
@@ -51,6 +52,13 @@ struct PotentialLaunch {
     std::int32_t out_ld, out_col0;
     std::int32_t out_chunk;
     long long out_chunk_stride;
+    // Multi-device sweep: when out_peer is set, chunk q goes to
+    // out_chunk_ptr[q] + (i - row_begin) * out_ld + k % out_chunk instead of
+    // out + q * out_chunk_stride + ... — the buffer of the device that owns
+    // sigma chunk q, written in place over peer memory (NVLink), so the
+    // potential kernel itself performs the V exchange.
+    int out_peer;
+    double* out_chunk_ptr[kMaxShards];
     // Polled CSR upload (host pipeline, unit weights, warp kernel): rows
     // [slab_bound[k], slab_bound[k+1]) may be read once slab_flags[k] != 0
     // (set by a copy after the slab's data on the copy stream); rows are
@@ -60,6 +68,16 @@ struct PotentialLaunch {
     int* slab_err;
     SigmaConsts c[kMaxSigmaPerLaunch];
 };
+
+#ifdef __CUDACC__
+// Address of (row i, launch sigma s) in the launch's output (see PotentialLaunch::out).
+__device__ __forceinline__ double* out_slot_ptr(const PotentialLaunch& P, const int i, const int s) {
+    const int k = P.out_col0 + s;
+    const int q = k / P.out_chunk;
+    double* base = P.out_peer ? P.out_chunk_ptr[q] : P.out + q * P.out_chunk_stride;
+    return base + static_cast<long long>(i - P.row_begin) * P.out_ld + (k - q * P.out_chunk);
+}
+#endif
 
 // Kernel launchers (kernels.cu). Return a cudaError_t as int.
 // Stream-ordered scratch comes from `pool` (a cudaMemPool_t that keeps its
@@ -121,6 +139,9 @@ struct KhopTable {
 };
 void fill_khop_table(KhopTable& t, int s, double sigma, int hop_cap, int exp_mode);
 int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTable& t, void* pool, void* stream);
+
+// SM count of the calling thread's current device (cached per device).
+int sm_count();
 
 // Launch accounting (kernels issued by the last C-ABI call).
 void count_launch(int k = 1);

@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 #include <utility>
@@ -195,13 +196,6 @@ __device__ __forceinline__ void first_run(Chain& ch, const double c, const Prefi
 // (neighbours and the row itself); K2 takes the first run from the prefix
 // table and every later run through the two-chain fast-forward.
 // ---------------------------------------------------------------------------
-// Output slot of row i, launch sigma s (see PotentialLaunch::out).
-__device__ __forceinline__ long long out_index(const PotentialLaunch& P, const int i, const int s) {
-    const int k = P.out_col0 + s;
-    const int q = k / P.out_chunk;
-    return q * P.out_chunk_stride + static_cast<long long>(i - P.row_begin) * P.out_ld + (k - q * P.out_chunk);
-}
-
 template <bool kFF, int kW>
 __global__ void __launch_bounds__(kBlock) potential_kernel(const __grid_constant__ PotentialLaunch P,
                                                            const PrefixTable T) {
@@ -323,7 +317,7 @@ __global__ void __launch_bounds__(kBlock) potential_kernel(const __grid_constant
         k = kk;
         pos = end;
     }
-    P.out[out_index(P, i, s)] = __dmul_rn(sc[0][s], __ddiv_rn(num.s, den.s));
+    *out_slot_ptr(P, i, s) = __dmul_rn(sc[0][s], __ddiv_rn(num.s, den.s));
 }
 
 // ---------------------------------------------------------------------------
@@ -455,12 +449,12 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
     };
 
 #if GQC_LANE_OUT_SMEM
-    __shared__ long long lane_out_s[32];
-    if (threadIdx.x < 32) lane_out_s[threadIdx.x] = out_index(P, P.row_begin, threadIdx.x);
+    __shared__ double* lane_out_s[32];
+    if (threadIdx.x < 32) lane_out_s[threadIdx.x] = out_slot_ptr(P, P.row_begin, min(static_cast<int>(threadIdx.x), S - 1));
     __syncthreads();
 #define lane_out (lane_out_s[lane])
 #else
-    const long long lane_out = out_index(P, P.row_begin, lane);  // this lane's sigma slot of row_begin
+    double* const lane_out = out_slot_ptr(P, P.row_begin, s);  // this lane's sigma slot of row_begin
 #endif
     const int nrows = R.limit ? *R.limit : P.row_end - P.row_begin;
     int grab = 0, left = 0;
@@ -604,7 +598,7 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
             }
         }
         if (lane < S)
-            P.out[lane_out + static_cast<long long>(i - P.row_begin) * P.out_ld] =
+            lane_out[static_cast<long long>(i - P.row_begin) * P.out_ld] =
                 __dmul_rn(sc[0][s], __ddiv_rn(num.s, den.s));
     }
 }
@@ -1010,15 +1004,18 @@ __global__ void resolve_error_kernel(int n, const int* __restrict__ term, unsign
 int grid_for(long long threads) { return static_cast<int>((threads + kBlock - 1) / kBlock); }
 
 // Side stream and fork/join events for companion launches, one set per parent
-// stream (calls into libgqc are serialized, so the map needs no lock of its own).
+// stream (calls on different devices run concurrently: the map is locked; a
+// parent stream belongs to one device, whose calls are serialized).
 struct SideStream {
     cudaStream_t stream = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
 };
 SideStream& side_for(cudaStream_t parent) {
+    static std::mutex mu;
     static std::map<std::pair<int, cudaStream_t>, SideStream> all;
     int dev = 0;
     cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
     SideStream& c = all[{dev, parent}];
     if (!c.stream) {
         cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking);
@@ -1058,12 +1055,7 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
     if (p.n_sigma >= kWarpKernelMinSigma) {
         // persistent warp-per-row kernel: one resident wave, rows scheduled
         // longest first through an atomic counter
-        static int num_sms = 0;
-        if (!num_sms) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-        }
+        const int num_sms = sm_count();
         const int rows = p.row_end - p.row_begin;
         auto pl = static_cast<cudaMemPool_t>(pool);
         std::size_t sort_bytes = 0;
@@ -1385,12 +1377,7 @@ int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nb
     cudaMemsetAsync(counts, 0, 4 * sizeof(int), st);
     mark_heavy_kernel<<<grid_for(rows), kBlock, 0, st>>>(off, row_begin, rows, items, counts, multi);
     count_launch(2);
-    static int num_sms = 0;
-    if (!num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int num_sms = sm_count();
     // thread = (row, sigma), sigma fastest: a neighbour's potentials for the
     // chunk's sigmas are one contiguous node-major line
     for (int c0 = 0; c0 < n_sigma; c0 += 32) {

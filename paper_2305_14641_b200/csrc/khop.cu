@@ -398,11 +398,6 @@ __global__ void khop_keys_kernel(const long long* __restrict__ off, const long l
     id[k] = k;
 }
 
-__device__ __forceinline__ long long out_slot(const PotentialLaunch& P, const int i, const int s) {
-    const int k = P.out_col0 + s;
-    const int q = k / P.out_chunk;
-    return q * P.out_chunk_stride + static_cast<long long>(i - P.row_begin) * P.out_ld + (k - q * P.out_chunk);
-}
 
 // Chunk of up to 32 merged events staged per warp for the batched walk:
 // classes 0 = hop 1 (CSR), 1 = hop 2; cnt(q, k) from the class ballots.
@@ -556,19 +551,11 @@ __global__ void __launch_bounds__(kWalkBlock, kWalkBlocksPerSM)
                 w_run(L);
             }
         }
-        if (lane < S) P.out[out_slot(P, i, s)] = __dmul_rn(sc[4][s], __ddiv_rn(num.s, den.s));
+        if (lane < S) *out_slot_ptr(P, i, s) = __dmul_rn(sc[4][s], __ddiv_rn(num.s, den.s));
     }
 }
 
-int num_sms() {
-    static int v = 0;
-    if (!v) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return v;
-}
+int num_sms() { return sm_count(); }
 
 }  // namespace
 

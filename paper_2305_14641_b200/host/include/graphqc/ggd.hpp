@@ -21,23 +21,34 @@ struct ClusterAssignment {
     std::vector<std::int32_t> cluster_index;
     std::vector<std::int32_t> centers;
     std::int32_t num_clusters = 0;
-    // Extension (not in the reference struct): modularity's intra-cluster
-    // weight of a unit-weight graph, counted on the device by cluster_batch
-    // (exact); modularity() then skips its O(nnz) row loop — only while
-    // cluster_index still hashes to intra_labels_hash (edited labels fall
-    // back to the full loop).
-    std::optional<double> intra_weight;
-    std::uint64_t intra_labels_hash = 0;
 };
-
-// Hash of a labelling that guards ClusterAssignment::intra_weight.
-std::uint64_t labels_hash(const std::vector<std::int32_t>& labels);
 
 SuccessorMap build_successors(const Graph& g, const PotentialField& pf);
 ClusterAssignment resolve_centers(const SuccessorMap& s);
+// `workers` (>= 1, as the reference validates) is the number of GPUs the rows
+// are sharded over: min(workers, max_gpus(), visible devices), one GPU for
+// graphs too small to gain from more (same bits for any count).
 ClusterAssignment cluster(const Graph& g, double sigma, int workers = 1);
-// One assignment per sigma from one batched device sweep. with_center = false
-// fills only cluster_index / num_clusters (all a sweep's metrics need).
-std::vector<ClusterAssignment> cluster_batch(const Graph& g, std::span<const double> sigmas, bool with_center = true);
+// One assignment per sigma from one batched device sweep over `workers` GPUs
+// (as cluster). with_center = false fills only cluster_index / num_clusters
+// (all a sweep's metrics need).
+std::vector<ClusterAssignment> cluster_batch(const Graph& g, std::span<const double> sigmas, bool with_center = true,
+                                             int workers = 1);
+
+// Upper bound on the GPUs a call shards over (default: every visible device;
+// the CLI's --gpus). Not a reference function: the reference's `workers` are
+// host threads.
+void set_max_gpus(int gpus);
+int max_gpus();
+
+namespace detail {
+// cluster_batch plus modularity's intra-cluster weight per sigma, counted
+// exactly on the device with the labels (unit-weight graphs; empty
+// otherwise). Used by run_sweep only, for the assignments it just made.
+std::vector<ClusterAssignment> cluster_batch_intra(const Graph& g, std::span<const double> sigmas, bool with_center,
+                                                   int workers, std::vector<double>* intra);
+// The device list of a call with `workers` workers on g.
+std::vector<std::int32_t> devices_for(const Graph& g, int workers);
+}  // namespace detail
 
 }  // namespace graphqc

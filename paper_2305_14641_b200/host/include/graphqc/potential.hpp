@@ -20,7 +20,8 @@ struct PotentialField {
 
 double node_potential(const Graph& g, std::int32_t node, double sigma);
 PotentialField compute_potentials(const Graph& g, double sigma);
-// `workers` is validated like the reference (>= 1); the field is the same bits.
+// `workers` (>= 1, validated like the reference) = GPUs the rows are sharded over
+// (see cluster in ggd.hpp); the field is the same bits for any count.
 PotentialField compute_potentials_parallel(const Graph& g, double sigma, int workers);
 // Batched: one field per sigma from one device pass over the CSR.
 std::vector<PotentialField> compute_potentials_batch(const Graph& g, std::span<const double> sigmas);

@@ -2,6 +2,7 @@
 #include "graphqc/potential.hpp"
 
 #include "device.hpp"
+#include "graphqc/ggd.hpp"
 
 namespace graphqc {
 
@@ -30,10 +31,17 @@ PotentialField compute_potentials(const Graph& g, double sigma) {
     return pf;
 }
 
+// potential.cpp:62-87: rows in contiguous blocks over `workers` workers —
+// here GPUs (detail::devices_for), each block's rows on its own device.
 PotentialField compute_potentials_parallel(const Graph& g, double sigma, int workers) {
     check_sigma(sigma);
     if (workers < 1) throw std::invalid_argument("workers must be at least 1");
-    return compute_potentials(g, sigma);
+    PotentialField pf{sigma, g.default_distance(), std::vector<double>(g.num_nodes())};
+    const gqc_csr c = detail::to_gqc(g);
+    const std::vector<std::int32_t> dev = detail::devices_for(g, workers);
+    detail::check(gqc_potentials_multi(&c, &sigma, 1, dev.data(), static_cast<std::int32_t>(dev.size()),
+                                       pf.values.data()));
+    return pf;
 }
 
 std::vector<PotentialField> compute_potentials_batch(const Graph& g, std::span<const double> sigmas) {

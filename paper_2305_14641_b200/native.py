@@ -36,6 +36,7 @@ KERNEL_FASTFWD = 0
 KERNEL_REPLAY = 1
 _OPT_EXP_MODE = 1
 _OPT_KERNEL = 2
+_OPT_GPUS = 5
 _OPT_DEVICE = 3
 _OPT_HOP_CAP = 4
 
@@ -79,6 +80,9 @@ def _load():
         "gqc_resolve_centers": [i32, P, P, P, P],
         "gqc_cluster_sweep": [P, P, i32, P, P, P, P, P],
         "gqc_cluster_sweep_intra": [P, P, i32, P, P, P, P, P, P],
+        "gqc_cluster_sweep_multi": [P, P, i32, P, i32, P, P, P, P, P, P],
+        "gqc_potentials_multi": [P, P, i32, P, i32, P],
+        "gqc_row_shards": [P, i32, P],
         "gqc_dev_potentials": [P, P, i32, i32, i32, P, P],
         "gqc_dev_potentials_packed": [P, P, i32, i32, i32, P, i32, i64, P],
         "gqc_dev_ggd": [P, P, i32, P, P, P, P, P, C.c_size_t, P],
@@ -177,6 +181,18 @@ def set_device(device: int):
     ...). The dev_* functions follow the device of the stream they are given.
     libgqc has its own CUDA runtime: torch.cuda.set_device does not reach it."""
     _check(_lib.gqc_set_option(_OPT_DEVICE, int(device)))
+
+
+def set_gpus(g: int):
+    """GQC_OPT_GPUS: the host-buffer sweeps (potentials, cluster_sweep, ...)
+    run row-sharded on devices GQC_OPT_DEVICE .. + g - 1; same bits for any g."""
+    _check(_lib.gqc_set_option(_OPT_GPUS, int(g)))
+
+
+def get_gpus() -> int:
+    v = np.zeros(1, dtype=np.int64)
+    _check(_lib.gqc_get_option(_OPT_GPUS, _ptr(v)))
+    return int(v[0])
 
 
 def set_hop_cap(k: int):
@@ -304,6 +320,47 @@ def cluster_sweep(g: Csr, sigmas: Sequence[float], want_v: bool = False, want_su
     else:
         out = [ClusterAssignment(center[q], ci[q], int(k[q])) for q in range(S)]
     return out, v, succ
+
+
+def row_shards(g: Csr, n_shards: int) -> np.ndarray:
+    """gqc_row_shards: bounds[0..n_shards] of the cost-balanced row blocks."""
+    out = np.zeros(n_shards + 1, dtype=np.int32)
+    cs = g.c_struct()
+    _check(_lib.gqc_row_shards(C.byref(cs), int(n_shards), _ptr(out)))
+    return out
+
+
+def cluster_sweep_multi(g: Csr, sigmas: Sequence[float], devices: Sequence[int], want_v: bool = False,
+                        want_succ: bool = False, want_center: bool = True, want_intra: bool = False):
+    """gqc_cluster_sweep_multi: the sweep row-sharded over `devices` (one
+    shard per entry; repeats put several shards on one device). Returns
+    (assignments, v, succ, intra) like cluster_sweep."""
+    s = np.ascontiguousarray(np.atleast_1d(np.asarray(sigmas, dtype=np.float64)))
+    d = np.ascontiguousarray(np.asarray(devices, dtype=np.int32))
+    S, n = len(s), g.n
+    v = np.empty((S, n)) if want_v else None
+    succ = np.empty((S, n), dtype=np.int32) if want_succ else None
+    center = np.empty((S, n), dtype=np.int32) if want_center else None
+    intra = np.zeros(S, dtype=np.int64) if want_intra else None
+    ci = np.empty((S, n), dtype=np.int32)
+    k = np.zeros(S, dtype=np.int32)
+    cs = g.c_struct()
+    _check(_lib.gqc_cluster_sweep_multi(C.byref(cs), _ptr(s), S, _ptr(d), len(d), _ptr(v), _ptr(succ),
+                                        _ptr(center), _ptr(ci), _ptr(k), _ptr(intra)))
+    if center is None:
+        out = [ClusterAssignment(None, ci[q], int(k[q]), centers=np.zeros(0, np.int32)) for q in range(S)]
+    else:
+        out = [ClusterAssignment(center[q], ci[q], int(k[q])) for q in range(S)]
+    return out, v, succ, intra
+
+
+def potentials_multi(g: Csr, sigmas: Sequence[float], devices: Sequence[int]) -> np.ndarray:
+    s = np.ascontiguousarray(np.atleast_1d(np.asarray(sigmas, dtype=np.float64)))
+    d = np.ascontiguousarray(np.asarray(devices, dtype=np.int32))
+    out = np.empty((len(s), g.n), dtype=np.float64)
+    cs = g.c_struct()
+    _check(_lib.gqc_potentials_multi(C.byref(cs), _ptr(s), len(s), _ptr(d), len(d), _ptr(out)))
+    return out
 
 
 def cluster(g: Csr, sigma: float, workers: int = 1) -> ClusterAssignment:

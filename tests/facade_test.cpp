@@ -77,22 +77,16 @@ int main(int argc, char** argv) {
         Graph g = from_text("a a\na b\n");
         CHECK(g.num_nodes() == 2 && g.num_edges() == 1 && neighbors(g, 0).size() == 1);
     }
-    // modularity with a device intra count (ClusterAssignment::intra_weight):
-    // used only while the labels still hash to what was counted
+    // modularity(g, assignment) always recomputes from the graph it is given
+    // (metrics.cpp:37-44): the device intra count is private to run_sweep
     {
         Graph g = from_text("0 1\n1 2\n2 0\n3 4\n4 5\n5 3\n2 3\n");
         ClusterAssignment a;
         a.cluster_index = {0, 0, 0, 1, 1, 1};
         a.num_clusters = 2;
-        const double plain = modularity(g, a);
-        a.intra_weight = 12.0;  // the true count of equal-label CSR entries
-        a.intra_labels_hash = labels_hash(a.cluster_index);
-        CHECK(modularity(g, a) == plain);
-        a.intra_weight = 999.0;  // a stale count for edited labels is ignored
-        a.cluster_index[3] = 0;
-        ClusterAssignment b = a;
-        b.intra_weight.reset();
-        CHECK(modularity(g, a) == modularity(g, b));
+        CHECK(modularity(g, a) == modularity(g, std::span<const std::int32_t>(a.cluster_index)));
+        Graph h = from_text("0 1\n1 2\n2 0\n3 4\n4 5\n5 3\n0 3\n1 4\n");
+        CHECK(modularity(h, a) != modularity(g, a));
     }
     // parse errors carry the line number
     CHECK(what_of("a b\nx\n").find("line 2") != std::string::npos);

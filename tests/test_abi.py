@@ -78,3 +78,34 @@ def test_no_cpu_fallback_without_device():
     g = N.Csr(np.array([0, 1, 2], np.int64), np.array([1, 0], np.int32), None, 10.0)
     with pytest.raises(N.CudaError, match="no CUDA device"):
         N.potentials(g, [1.0])
+
+
+def test_row_shards_partition_cpu():
+    """gqc_row_shards (no device needed): contiguous blocks covering every row,
+    balanced by deg + 16 per row for the fast-forward kernel, and the
+    reference's equal blocks w*floor(n/k) + min(w, n mod k)
+    (potential.cpp:70-74) for the dense replay."""
+    import numpy as np
+
+    from bench_tools import graphgen
+    from paper_2305_14641_b200 import native as N
+    graphgen.build()
+    off, nbr = graphgen.rmat(scale=16)
+    csr = N.Csr(off, nbr, None, 10.0)
+    n = len(off) - 1
+    cost = np.diff(off) + 16
+    for k in (1, 2, 3, 8, 32):
+        b = N.row_shards(csr, k)
+        assert b[0] == 0 and b[-1] == n and np.all(np.diff(b) >= 0)
+        per = np.array([cost[b[r]:b[r + 1]].sum() for r in range(k)])
+        assert per.max() <= cost.sum() / k + cost.max()
+    N.set_kernel(N.KERNEL_REPLAY)
+    try:
+        for k in (3, 7):
+            b = N.row_shards(csr, k)
+            assert list(b) == [w * (n // k) + min(w, n % k) for w in range(k)] + [n]
+    finally:
+        N.set_kernel(N.KERNEL_FASTFWD)
+    import pytest
+    with pytest.raises(ValueError):
+        N.row_shards(csr, 33)
