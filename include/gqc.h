@@ -175,7 +175,7 @@ gqc_status gqc_potentials_multi(const gqc_csr* g, const double* sigmas, int32_t 
 
 /* Row blocks of a multi-device sweep: bounds[0] = 0 <= bounds[1] <= ... <=
  * bounds[n_shards] = n, shard r = rows [bounds[r], bounds[r+1]). Balanced by
- * the fast-forward kernel's cost per row (~ degree + 16), i.e. by an nnz
+ * the fast-forward kernel's cost per row (~ degree + 4), i.e. by an nnz
  * prefix over offsets; equal blocks w*floor(n/k) + min(w, n mod k)
  * (potential.cpp:70-74) under GQC_KERNEL_REPLAY, whose rows all cost n. */
 gqc_status gqc_row_shards(const gqc_csr* g, int32_t n_shards, int32_t* bounds);

@@ -934,7 +934,7 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
 // balanced by the fast-forward kernel's cost, ~ deg(i) + kRowCost per row.
 // The reference's equal blocks (potential.cpp:70-74) balance its O(N) rows
 // only; they are kept for the dense replay, whose rows all cost N.
-constexpr long long kRowCost = 16;
+constexpr long long kRowCost = 4;
 
 static std::vector<int> row_shards(const std::int64_t* off, int n, int shards, int kernel) {
     std::vector<int> b(shards + 1, n);

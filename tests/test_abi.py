@@ -82,7 +82,7 @@ def test_no_cpu_fallback_without_device():
 
 def test_row_shards_partition_cpu():
     """gqc_row_shards (no device needed): contiguous blocks covering every row,
-    balanced by deg + 16 per row for the fast-forward kernel, and the
+    balanced by deg + 4 per row for the fast-forward kernel, and the
     reference's equal blocks w*floor(n/k) + min(w, n mod k)
     (potential.cpp:70-74) for the dense replay."""
     import numpy as np
@@ -93,7 +93,7 @@ def test_row_shards_partition_cpu():
     off, nbr = graphgen.rmat(scale=16)
     csr = N.Csr(off, nbr, None, 10.0)
     n = len(off) - 1
-    cost = np.diff(off) + 16
+    cost = np.diff(off) + 4
     for k in (1, 2, 3, 8, 32):
         b = N.row_shards(csr, k)
         assert b[0] == 0 and b[-1] == n and np.all(np.diff(b) >= 0)
