@@ -163,10 +163,11 @@ struct PotScratch {
 struct ShardBufs {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev_pot = nullptr;
-    DevBuf v, v_sm, succ, center, ci, nc, ws, intra, send;
+    DevBuf v, v_sm, succ, center, ci, nc, ws, intra, send, err;
     PotScratch scr;
     int* nc_host = nullptr;  // pinned counts staging
     int nc_host_cap = 0;
+    int* err_host = nullptr;  // pinned: GGD cycle flag readback
 };
 
 struct DeviceCtx {
@@ -178,8 +179,9 @@ struct DeviceCtx {
     cudaEvent_t ev[16] = {};
     cudaEvent_t slab_done[4] = {};
     cudaMemPool_t pool = nullptr;  // stream-ordered scratch that keeps its memory
-    DevBuf off, nbr, w, v_nm, v_sm, succ, center, ci, nc, ws, intra;
+    DevBuf off, nbr, w, v_nm, v_sm, succ, center, ci, nc, ws, intra, err;
     PotScratch scr;
+    int* err_host = nullptr;  // pinned: GGD cycle flag readback
     int* nc_host = nullptr;  // pinned staging for per-sigma counts (cudaHostAlloc)
     int nc_host_cap = 0;
     DevBuf slab_sync;            // polled upload: [4] slab flags, [4] error word
@@ -210,6 +212,16 @@ int* pinned_counts_buf(int*& buf, int& cap, int n) {
     return buf;
 }
 int* pinned_counts(DeviceCtx& C, int n) { return pinned_counts_buf(C.nc_host, C.nc_host_cap, n); }
+
+// Device word the bounded chase sets when a successor map has a cycle
+// (launch_chase), cleared on `st`; its pinned readback slot.
+int* ggd_err_word(DevBuf& buf, int*& host, cudaStream_t st) {
+    int* d = buf.get<int>(1);
+    cuda_check(cudaMemsetAsync(d, 0, sizeof(int), st), "clear error word");
+    if (!host) cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&host), sizeof(int), cudaHostAllocDefault), "cudaHostAlloc");
+    *host = 0;
+    return d;
+}
 
 // libgqc carries its own (static) CUDA runtime, whose current device is not
 // the caller's (torch.cuda.set_device does not reach it). Every call binds it
@@ -331,6 +343,15 @@ void host_exp_table(const double* d2, long long count, const std::vector<double>
 // Potentials of rows [row_begin, row_end) into v_nm[(i-row_begin)*S + s]
 // (device), for a device-resident CSR. host_w: the same weights on the host
 // (only consulted for weighted graphs), or nullptr to fetch what is needed.
+long long slab_timeout_ms() {  // GQC_SLAB_TIMEOUT_MS: polled-upload flag wait before GQC_ECUDA
+    static const long long ms = [] {
+        const char* e = std::getenv("GQC_SLAB_TIMEOUT_MS");
+        const long long v = e ? std::atoll(e) : 0;
+        return v > 0 ? v : 5000ll;
+    }();
+    return ms;
+}
+
 struct SlabSync {  // polled CSR upload (see PotentialLaunch::slab_flags)
     const int* flags = nullptr;
     int bound[5] = {};
@@ -420,6 +441,7 @@ void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S,
             P.slab_flags = sync->flags;
             for (int k = 0; k < 5; ++k) P.slab_bound[k] = sync->bound[k];
             P.slab_err = sync->err;
+            P.slab_timeout_ns = slab_timeout_ms() * 1000000ll;
         }
         std::vector<double> neg_inv(Sc);
         for (int s = 0; s < Sc; ++s) {
@@ -805,8 +827,7 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
                     cuda_check(cudaMemcpyAsync(nbr + a2, g->nbr + a2, (b2 - a2) * sizeof(std::int32_t),
                                                cudaMemcpyHostToDevice, cs),
                                "copy nbr");
-                cuda_check(cudaMemcpyAsync(flags + k, C.slab_host + k, sizeof(int), cudaMemcpyHostToDevice, cs),
-                           "set slab flag");
+                cuda_check(launch_set_flag(flags + k, cs), "set slab flag");
             }
             cuda_check(cudaStreamWaitEvent(st, C.ev[0], 0), "wait");
             SlabSync sync;
@@ -875,6 +896,7 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
         const bool overlap = host_pinned(cluster_index_out) && (!center_out || host_pinned(center_out)) &&
                              (!succ_out || host_pinned(succ_out));
         int* nc_stage = pinned_counts(C, n_sigma);
+        int* d_err = ggd_err_word(C.err, C.err_host, st);
         int ev_i = 9;
         auto download = [&](int s0, int Sc) {
             const std::size_t o = static_cast<std::size_t>(s0) * n, c = static_cast<std::size_t>(Sc) * n;
@@ -895,7 +917,7 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
             cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, s0, Sc, 0, n, ds + o, 1, n, nnz, C.pool, st,
                                          order.get()),
                        "successor kernel");
-            cuda_check(launch_chase(n, Sc, ds + o, dc + o, st, ws), "chase kernel");
+            cuda_check(launch_chase(n, Sc, ds + o, dc + o, st, ws, d_err), "chase kernel");
             cuda_check(launch_labels(n, Sc, dc + o, dci + o, dnc + s0, ws, wsb, st, true), "label kernels");
             if (intra_out)
                 cuda_check(launch_intra_counts(n, Sc, d.offsets, d.nbr, dci + o, d_intra + s0, st), "intra counts");
@@ -922,9 +944,11 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
         if (intra_out)
             cuda_check(cudaMemcpyAsync(intra_out, d_intra, n_sigma * sizeof(long long), cudaMemcpyDeviceToHost, st),
                        "copy intra counts");
+        cuda_check(cudaMemcpyAsync(C.err_host, d_err, sizeof(int), cudaMemcpyDeviceToHost, st), "copy error word");
         cuda_check(cudaStreamSynchronize(cs), "cluster sweep (copies)");
         cuda_check(cudaStreamSynchronize(st), "cluster sweep");
         if (polled && C.slab_host[4]) fail(GQC_ECUDA, "CSR upload did not arrive (polled slab flag timeout)");
+        if (*C.err_host) fail(GQC_ECYCLE, "successor map contains a cycle");  // ggd.cpp:41
         std::copy(nc_stage, nc_stage + n_sigma, num_clusters_out);
     }
 }
@@ -1106,8 +1130,10 @@ static void sweep_multi_impl(const gqc_csr* g, const double* sigmas, int S, cons
         cuda_check(launch_successors(n, dg.offsets, dg.nbr, V[q], chunk, 0, Sq, 0, n, ds, 1, n, nnz, X.pool, st,
                                      order.get()),
                    "successor kernel");
-        cuda_check(launch_chase(n, Sq, ds, dc, st, ws), "chase kernel");
+        int* d_err = ggd_err_word(Bq.err, Bq.err_host, st);
+        cuda_check(launch_chase(n, Sq, ds, dc, st, ws, d_err), "chase kernel");
         cuda_check(launch_labels(n, Sq, dc, dci, dnc, ws, wsb, st, true), "label kernels");
+        cuda_check(cudaMemcpyAsync(Bq.err_host, d_err, sizeof(int), cudaMemcpyDeviceToHost, st), "copy error word");
         if (intra_out)
             cuda_check(launch_intra_counts(n, Sq, dg.offsets, dg.nbr, dci, Bq.intra.get<long long>(Sq), st),
                        "intra counts");
@@ -1146,8 +1172,11 @@ static void sweep_multi_impl(const gqc_csr* g, const double* sigmas, int S, cons
         cuda_check(cudaSetDevice(devices[r]), "cudaSetDevice");
         cuda_check(cudaStreamSynchronize(B[r]->stream), "multi-device sweep");
     }
-    if (!potentials_only)
+    if (!potentials_only) {
+        for (int q = 0; q < nchunks; ++q)
+            if (*B[q]->err_host) fail(GQC_ECYCLE, "successor map contains a cycle");  // ggd.cpp:41
         for (int q = 0; q < nchunks; ++q) std::copy(B[q]->nc_host, B[q]->nc_host + s_count(q), nc_out + s_begin(q));
+    }
 }
 
 // Devices of the host-buffer entry points: GQC_OPT_DEVICE .. + GQC_OPT_GPUS - 1.

@@ -66,6 +66,7 @@ struct PotentialLaunch {
     const int* slab_flags;
     std::int32_t slab_bound[5];
     int* slab_err;
+    long long slab_timeout_ns;  // GQC_SLAB_TIMEOUT_MS (default 5000)
     SigmaConsts c[kMaxSigmaPerLaunch];
 };
 
@@ -112,14 +113,18 @@ int launch_successors(std::int32_t n, const std::int64_t* offsets, const std::in
 int launch_intra_counts(std::int32_t n, std::int32_t n_sigma, const std::int64_t* offsets, const std::int32_t* nbr,
                         const std::int32_t* ci_sm, long long* out, void* stream);
 int launch_transpose_i32(const std::int32_t* in, std::int32_t n, std::int32_t n_sigma, std::int32_t* out, void* stream);
-// labels_workspace (optional): launch_labels' workspace; the chase then writes
-// the center flags there and launch_labels must be called with flags_ready.
+// labels_workspace: launch_labels' workspace (required); the chase writes the
+// center flags there (call launch_labels with flags_ready) and keeps its
+// status words there. err (optional, device): set to 1 if a map has a cycle
+// (bounded chase + pointer jumping, see chase_kernel).
 int launch_chase(std::int32_t n, std::int32_t n_sigma, const std::int32_t* succ_sm, std::int32_t* center_sm,
-                 void* stream, void* labels_workspace = nullptr);
+                 void* stream, void* labels_workspace, std::int32_t* err = nullptr);
 int launch_labels(std::int32_t n, std::int32_t n_sigma, const std::int32_t* center_sm, std::int32_t* cluster_index_sm,
                   std::int32_t* num_clusters, void* workspace, std::size_t ws_bytes, void* stream,
                   bool flags_ready = false);
 std::size_t labels_workspace_bytes(std::int32_t n, std::int32_t n_sigma);
+// Polled upload: release-store 1 to a slab flag on the copy stream (after the slab's copy).
+int launch_set_flag(int* flag, void* stream);
 int launch_transpose(const double* v_nm, std::int32_t n, std::int32_t n_sigma, double* v_sm, void* stream);
 // Checked resolve for arbitrary successor maps: writes center/cluster_index,
 // returns status via *err_kind (0 ok, 1 out of range, 2 cycle) on the host.

@@ -19,12 +19,14 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <string>
 #include <vector>
 #include <utility>
 
+#include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -36,9 +38,18 @@
 #ifndef GQC_WALK2
 #define GQC_WALK2 1
 #endif
+// GQC_LEAN=1: W runs of the warp kernel (unit weights) take a vote-guarded
+// fast path — one exact fma per chain when every lane's run stays inside
+// its cached binade — and fall back to the general ff_run only for the lanes
+// that cross (see ff_lean2).
+#ifndef GQC_LEAN
+#define GQC_LEAN 1
+#endif
 #ifndef GQC_LANE_OUT_SMEM
 #define GQC_LANE_OUT_SMEM 1
 #endif
+
+namespace cg = cooperative_groups;
 
 namespace gqc {
 namespace {
@@ -141,11 +152,13 @@ struct RowSched {
 constexpr int kMaxHubs = 16;
 constexpr int kHubSmemBytes = 196 * 1024;
 
-__global__ void hub_split_kernel(const int* __restrict__ deg_sorted, int rows, long long threshold,
+// deg_mask: the polled upload's sort keys carry the slab in bits 24+ (see
+// row_degree_kernel); only the degree bits are compared with the threshold.
+__global__ void hub_split_kernel(const int* __restrict__ deg_sorted, int rows, long long threshold, int deg_mask,
                                  int* __restrict__ hub_count, int* __restrict__ main_counter,
                                  int* __restrict__ hub_counter) {
     int h = 0;
-    while (h < kMaxHubs && h < rows && deg_sorted[h] > threshold) ++h;
+    while (h < kMaxHubs && h < rows && (deg_sorted[h] & deg_mask) > threshold) ++h;
     *hub_count = h;
     *main_counter = h;
     *hub_counter = 0;
@@ -339,7 +352,7 @@ constexpr int kBatchMinDegree = GQC_BATCH_MIN_DEGREE;  // padded: no bank confli
 // the flag of row i's slab; a flag that never arrives sets *slab_err after
 // ~5 s instead of hanging the GPU.
 __device__ __noinline__ void wait_slab(const int* flags, const int b1, const int b2, const int b3, int* err,
-                                       const int i) {
+                                       const int i, const unsigned long long timeout_ns) {
     const int slab = (i >= b1) + (i >= b2) + (i >= b3);
     if ((threadIdx.x & 31) == 0) {
         unsigned long long t0;
@@ -350,7 +363,7 @@ __device__ __noinline__ void wait_slab(const int* flags, const int b1, const int
             if (f || *static_cast<volatile int*>(err)) break;  // arrived, or another warp timed out
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            if (t - t0 > 5000000000ull) {
+            if (t - t0 > timeout_ns) {
                 atomicExch(err, 1);
                 break;
             }
@@ -359,6 +372,49 @@ __device__ __noinline__ void wait_slab(const int* flags, const int b1, const int
     }
     __syncwarp();
     __threadfence();
+}
+
+// Both chains of a W run of length L > 0 in the warp kernel (lane = sigma).
+// The common case — every lane's run ends inside the binade its chain has
+// cached, outside the tie binade — is one exact fma per chain and a warp vote;
+// only then the general ff_run walks the lanes that cross (binade crossings,
+// real adds, tie parity). Same result as ff_run2 bit for bit: with a valid
+// cache, flags == kJump and t < top, ff_run's first step is exactly s = t, and
+// otherwise ff_run runs from the unchanged state.
+__device__ __forceinline__ void ff_lean2(Chain& a, const double ca, Chain& b, const double cb, const int L) {
+    const double Ld = static_cast<double>(L);
+    const double ta = __fma_rn(Ld, a.inc, a.s);
+    const double tb = __fma_rn(Ld, b.inc, b.s);
+    const bool oka = a.flags == kJump && ta < a.top;
+    const bool okb = b.flags == kJump && tb < b.top;
+    a.s = oka ? ta : a.s;
+    b.s = okb ? tb : b.s;
+    if (__any_sync(0xffffffffu, !(oka && okb))) {
+        if (!oka) ff_run(a, ca, L);
+        if (!okb) ff_run(b, cb, L);
+    }
+}
+
+// CSR neighbour load of the warp kernel. Under the polled upload the copy
+// engine is still writing nbr while the kernel runs, so those loads are
+// coherent (ld.relaxed.gpu, ordered after the slab flag's acquire) instead of
+// the read-only path (ld.global.nc requires data constant for the kernel's
+// lifetime).
+__device__ __forceinline__ int load_nbr(const PotentialLaunch& P, const long long k) {
+    if (P.slab_flags) {
+        int v;
+        asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(P.nbr + k) : "memory");
+        return v;
+    }
+    return __ldg(P.nbr + k);
+}
+
+// Release-store of a polled-upload slab flag, launched on the copy stream
+// right after the slab's copy: stream order makes the copy happen-before this
+// kernel, and the release store publishes it to the potential kernel's
+// acquire load (wait_slab).
+__global__ void set_flag_kernel(int* flag) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(1) : "memory");
 }
 
 template <bool kFF, int kW>
@@ -437,7 +493,10 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
                     ch.top = 0.0;
                 }
             } else {
-#if GQC_WALK2
+#if GQC_LEAN
+                if constexpr (kW == kUnit) ff_lean2(num, pW, den, eW, L);
+                else ff_walk2(num, pW, den, eW, L);
+#elif GQC_WALK2
                 ff_walk2(num, pW, den, eW, L);
 #else
                 ff_run2(num, pW, den, eW, L);
@@ -470,7 +529,9 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
         const int i = R.order[grab];
         ++grab;
         --left;
-        if (P.slab_flags) wait_slab(P.slab_flags, P.slab_bound[1], P.slab_bound[2], P.slab_bound[3], P.slab_err, i);
+        if (P.slab_flags)
+            wait_slab(P.slab_flags, P.slab_bound[1], P.slab_bound[2], P.slab_bound[3], P.slab_err, i,
+                      static_cast<unsigned long long>(P.slab_timeout_ns));
         const long long kbeg = P.offsets[i], kend = P.offsets[i + 1];
         Chain num, den;
         num.s = 0.0; num.top = 0.0; num.inc = 0.0; num.f_tie = tie_num; num.flags = 0;
@@ -539,7 +600,7 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
             };
             for (long long base = kbeg; base < kend; base += 32) {
                 const int cnt = static_cast<int>(min(32ll, kend - base));
-                const int my = lane < cnt ? __ldg(P.nbr + base + lane) : n;
+                const int my = lane < cnt ? load_nbr(P, base + lane) : n;
                 __syncwarp();
                 cols[lane] = my;
                 __syncwarp();
@@ -570,7 +631,7 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
             // neighbours in chunks of 32: one coalesced load, then shuffles
             for (long long base = kbeg; base < kend; base += 32) {
                 const int cnt = static_cast<int>(min(32ll, kend - base));
-                const int my = lane < cnt ? __ldg(P.nbr + base + lane) : n;
+                const int my = lane < cnt ? load_nbr(P, base + lane) : n;
                 double myw = 1.0;
                 if constexpr (kW != kUnit) myw = lane < cnt ? __ldg(P.w + base + lane) : 1.0;
                 for (int j = 0; j < cnt; ++j) {
@@ -903,22 +964,67 @@ __global__ void transpose_i32_kernel(const int* __restrict__ in, int n, int S, i
 // succ; every thread follows pointers through center[], which other threads
 // overwrite with roots as they finish (any value read is an ancestor, so the
 // result is exact; finished neighbours shorten the walk). Maps built by K3
-// strictly decrease (v, id) along a chain, so every walk terminates.
+// strictly decrease (v, id) along a chain, so every walk terminates — but a
+// long monotone chain would cost one thread O(depth) dependent loads, so a
+// walk stops after kChaseSteps, leaves the ancestor it reached and counts
+// itself pending; jump_kernel then finishes by pointer jumping in at most
+// ceil(log2 n) + 2 synchronous rounds (or reports a cycle, ggd.cpp:41).
 // With flag != nullptr it also writes the center flags of K5a (flag[b + i] =
-// root == i), saving the label pass its read of center[].
-__global__ void __launch_bounds__(kBlock) chase_kernel(int n, int* __restrict__ center, int* __restrict__ flag) {
+// root == i, i.e. succ[i] == i: roots are known before any chasing).
+constexpr int kChaseSteps = 256;
+
+__global__ void __launch_bounds__(kBlock) chase_kernel(int n, int* __restrict__ center, int* __restrict__ flag,
+                                                       int* __restrict__ pending) {
     const int i = blockIdx.x * kBlock + threadIdx.x;
     if (i >= n) return;
     const long long b = static_cast<long long>(blockIdx.y) * n;
     int* c = center + b;
     int x = c[i];
-    for (;;) {
+    if (flag) flag[b + i] = x == i ? 1 : 0;
+    for (int step = 0;; ++step) {
         const int y = c[x];
         if (y == x) break;
         x = y;
+        if (step == kChaseSteps) {
+            atomicAdd(pending, 1);
+            break;
+        }
     }
     c[i] = x;
-    if (flag) flag[b + i] = x == i ? 1 : 0;
+}
+
+// Pointer jumping over every (sigma, node) of center[] until all point at
+// roots; does nothing (one launch, all blocks return at once) when no chase
+// hit its step bound. Cooperative launch: rounds are separated by grid syncs,
+// so each round at least halves every remaining distance (in-place updates
+// only jump further). A map still unresolved after `rounds` rounds has a
+// cycle: *err = 1.
+__global__ void __launch_bounds__(kBlock) jump_kernel(int n, int S, int* __restrict__ center,
+                                                      int* __restrict__ status, int rounds, int* __restrict__ err) {
+    if (*reinterpret_cast<volatile int*>(status) == 0) return;  // no pending chase (uniform across the grid)
+    cg::grid_group grid = cg::this_grid();
+    const long long total = static_cast<long long>(n) * S;
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    const long long t0 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool done = false;
+    for (int r = 0; r < rounds && !done; ++r) {
+        int* cnt = status + 1 + (r % 3);
+        if (t0 == 0) status[1 + ((r + 1) % 3)] = 0;  // last read before the previous round's sync
+        int changed = 0;
+        for (long long t = t0; t < total; t += stride) {
+            const long long b = t - t % n;
+            const int x = center[t];
+            const int y = center[b + x];
+            if (y != x) {
+                center[t] = y;
+                ++changed;
+            }
+        }
+        if (changed) atomicAdd(cnt, changed);
+        grid.sync();
+        done = *reinterpret_cast<volatile int*>(cnt) == 0;
+    }
+    if (!done && t0 == 0 && err) atomicExch(err, 1);
 }
 
 // K5a: center flags for the dense relabel scan (flag[S*n] = 0 terminator).
@@ -1065,7 +1171,10 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
         const std::size_t arr = ((static_cast<std::size_t>(rows) * sizeof(int)) + 255) & ~static_cast<std::size_t>(255);
         void* sched = nullptr;
         cudaError_t e = cudaMallocFromPoolAsync(&sched, 4 * arr + sort_bytes + 256, pl, st);
-        if (e != cudaSuccess) return e;
+        if (e != cudaSuccess) {
+            if (mem) cudaFreeAsync(mem, st);
+            return e;
+        }
         char* b = static_cast<char*>(sched);
         int* deg_in = reinterpret_cast<int*>(b);
         int* deg_out = reinterpret_cast<int*>(b + arr);
@@ -1079,7 +1188,11 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
         count_launch();
         e = cub::DeviceRadixSort::SortPairsDescending(temp, sort_bytes, deg_in, deg_out, id_in, id_out, rows, 0, 32, st);
         count_launch(2);
-        if (e != cudaSuccess) return e;
+        if (e != cudaSuccess) {  // no scratch leaks on the error path
+            cudaFreeAsync(sched, st);
+            if (mem) cudaFreeAsync(mem, st);
+            return e;
+        }
         // hub rows (see hub_split_kernel): longer than ~1/4096 of the entries.
         // The unit-weight fast-forward walks long rows with batched in-binade
         // jumps (walk_events), so a hub costs it ~10^2 steps and no hub gets
@@ -1088,7 +1201,8 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
         int* hub_counter = counter + 2;
         const bool hubs = !(ff && p.weight_mode == kUnit);
         const long long threshold = hubs ? std::max<long long>(4096, p.nnz / 4096) : (1ll << 62);
-        hub_split_kernel<<<1, 1, 0, st>>>(deg_out, rows, threshold, hub_count, counter, hub_counter);
+        hub_split_kernel<<<1, 1, 0, st>>>(deg_out, rows, threshold, p.slab_flags ? 0xffffff : -1, hub_count, counter,
+                                          hub_counter);
         count_launch();
         const RowSched R{id_out, counter, nullptr};
         const RowSched Rh{id_out, hub_counter, hub_count};
@@ -1383,13 +1497,21 @@ int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nb
     for (int c0 = 0; c0 < n_sigma; c0 += 32) {
         const int Sc = std::min(32, n_sigma - c0);
         const SuccOut O{out + c0 * out_col, out_row, out_col};
-        const long long threads = static_cast<long long>(rows) * Sc;
-        if (threads >= (1ll << 31) - kBlock) return cudaErrorInvalidValue;  // 32-bit thread ids
-        if (co && co->dir)
-            successors_class_kernel<<<grid_for(static_cast<long long>(rows) * 32), kBlock, 0, st>>>(
-                off, nbr, v, ld, s0 + c0, Sc, row_begin, rows, O, *co);
-        else
-            successors_kernel<<<grid_for(threads), kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, rows, O);
+        // light rows: the kernels index threads in 32 bits, so the row range
+        // goes in sub-launches of fewer than 2^31 threads (graphs of ~67M+
+        // nodes at 32 sigmas), each with its output moved to its first row
+        const long long per = ((1ll << 31) - 2 * kBlock) / 32;
+        for (long long r0 = 0; r0 < rows; r0 += per) {
+            const int rr = static_cast<int>(std::min<long long>(per, rows - r0));
+            const SuccOut Or{O.out + r0 * out_row, out_row, out_col};
+            const int rb = row_begin + static_cast<int>(r0);
+            if (co && co->dir)
+                successors_class_kernel<<<grid_for(static_cast<long long>(rr) * 32), kBlock, 0, st>>>(
+                    off, nbr, v, ld, s0 + c0, Sc, rb, rr, Or, *co);
+            else
+                successors_kernel<<<grid_for(static_cast<long long>(rr) * Sc), kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0,
+                                                                                              Sc, rb, rr, Or);
+        }
         successors_heavy_kernel<<<num_sms * 8, kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, items, counts,
                                                                  part_v, part_i, O);
         successors_combine_kernel<<<num_sms * 2, kBlock, 0, st>>>(multi, counts, part_v, part_i, Sc, row_begin, O);
@@ -1406,51 +1528,99 @@ int launch_transpose_i32(const std::int32_t* in, int n, int n_sigma, std::int32_
     return cudaGetLastError();
 }
 
+namespace {
+// launch_labels' workspace: [status 256 B][flag][scan][CUB temp]. status[0]:
+// chases that hit their step bound; status[1..3]: jump_kernel's round counters.
+struct LabelsWs {
+    int* status;
+    int* flag;
+    int* scan;
+    void* temp;
+    std::size_t temp_bytes;
+};
+std::size_t align256(std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); }
+std::size_t scan_temp_bytes(long long items) {
+    std::size_t temp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, temp, static_cast<const int*>(nullptr), static_cast<int*>(nullptr), items);
+    return temp;
+}
+LabelsWs labels_ws(void* workspace, std::size_t ws_bytes, int n, int n_sigma) {
+    const long long items = static_cast<long long>(n) * n_sigma + 1;
+    char* w = static_cast<char*>(workspace);
+    LabelsWs L;
+    L.status = reinterpret_cast<int*>(w);
+    L.flag = reinterpret_cast<int*>(w + 256);
+    L.scan = reinterpret_cast<int*>(w + 256 + align256(sizeof(int) * items));
+    L.temp = w + 256 + 2 * align256(sizeof(int) * items);
+    L.temp_bytes = ws_bytes - 256 - 2 * align256(sizeof(int) * items);
+    return L;
+}
+int jump_grid() {  // co-resident blocks of jump_kernel (cooperative launch), per device
+    static std::atomic<int> cache[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    int v = cache[dev].load();
+    if (!v) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jump_kernel, kBlock, 0);
+        v = std::max(1, per_sm) * sm_count();
+        cache[dev].store(v);
+    }
+    return v;
+}
+}  // namespace
+
 int launch_chase(int n, int n_sigma, const std::int32_t* succ_sm, std::int32_t* center_sm, void* stream,
-                 void* labels_workspace) {
+                 void* labels_workspace, std::int32_t* err) {
     auto st = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaSuccess;
     if (succ_sm != center_sm)
         e = cudaMemcpyAsync(center_sm, succ_sm, sizeof(int) * static_cast<size_t>(n) * n_sigma,
                             cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return e;
-    int* flag = static_cast<int*>(labels_workspace);  // launch_labels' flag array (first in its workspace)
-    if (flag) {
-        e = cudaMemsetAsync(flag + static_cast<long long>(n) * n_sigma, 0, sizeof(int), st);  // scan terminator
-        if (e != cudaSuccess) return e;
-    }
-    chase_kernel<<<dim3(grid_for(n), n_sigma), kBlock, 0, st>>>(n, center_sm, flag);
+    if (!labels_workspace) return cudaErrorInvalidValue;
+    const LabelsWs L = labels_ws(labels_workspace, 0, n, n_sigma);
+    // status words and the scan terminator (flag[n * n_sigma])
+    e = cudaMemsetAsync(L.status, 0, 4 * sizeof(int), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(L.flag + static_cast<long long>(n) * n_sigma, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    chase_kernel<<<dim3(grid_for(n), n_sigma), kBlock, 0, st>>>(n, center_sm, L.flag, L.status);
+    count_launch();
+    int rounds = 2;
+    while ((1ll << (rounds - 2)) < n) ++rounds;  // ceil(log2 n) + 2
+    void* args[] = {&n, &n_sigma, &center_sm, const_cast<int**>(&L.status), &rounds, &err};
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jump_kernel), dim3(jump_grid()), dim3(kBlock), args, 0, st);
+    count_launch();
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+int launch_set_flag(int* flag, void* stream) {
+    set_flag_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flag);
     count_launch();
     return cudaGetLastError();
 }
 
 std::size_t labels_workspace_bytes(int n, int n_sigma) {
     const long long items = static_cast<long long>(n) * n_sigma + 1;
-    std::size_t temp = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, temp, static_cast<const int*>(nullptr), static_cast<int*>(nullptr),
-                                  items);
-    auto align = [](std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); };
-    return 2 * align(sizeof(int) * items) + align(temp);
+    return 256 + 2 * align256(sizeof(int) * items) + align256(scan_temp_bytes(items));
 }
 
 int launch_labels(int n, int n_sigma, const std::int32_t* center_sm, std::int32_t* ci_sm, std::int32_t* num_clusters,
                   void* workspace, std::size_t ws_bytes, void* stream, bool flags_ready) {
     auto st = static_cast<cudaStream_t>(stream);
     const long long items = static_cast<long long>(n) * n_sigma + 1;
-    auto align = [](std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); };
-    char* w = static_cast<char*>(workspace);
-    int* flag = reinterpret_cast<int*>(w);
-    int* scan = reinterpret_cast<int*>(w + align(sizeof(int) * items));
-    void* temp = w + 2 * align(sizeof(int) * items);
-    std::size_t temp_bytes = ws_bytes - 2 * align(sizeof(int) * items);
+    const LabelsWs L = labels_ws(workspace, ws_bytes, n, n_sigma);
     if (!flags_ready) {  // else launch_chase wrote them
-        center_flags_kernel<<<grid_for(items), kBlock, 0, st>>>(n, n_sigma, center_sm, flag);
+        center_flags_kernel<<<grid_for(items), kBlock, 0, st>>>(n, n_sigma, center_sm, L.flag);
         count_launch();
     }
-    cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, flag, scan, items, st);
+    std::size_t temp_bytes = L.temp_bytes;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(L.temp, temp_bytes, L.flag, L.scan, items, st);
     count_launch(2);  // CUB: init + scan kernels
     if (e != cudaSuccess) return e;
-    relabel_kernel<<<dim3(grid_for(n), n_sigma), kBlock, 0, st>>>(n, center_sm, scan, ci_sm, num_clusters);
+    relabel_kernel<<<dim3(grid_for(n), n_sigma), kBlock, 0, st>>>(n, center_sm, L.scan, ci_sm, num_clusters);
     count_launch();
     return cudaGetLastError();
 }

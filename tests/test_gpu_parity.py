@@ -375,8 +375,9 @@ def test_pipelined_sweep_weighted_odd_n_sampled_oracle():
 
 
 def test_hub_rows_heavy_argmin_and_scheduling():
-    # hubs above the heavy-row threshold (1024) take the block-parallel argmin
-    # and the longest-first row schedule; everything still matches the oracle
+    # hubs above the heavy-row threshold (kHeavyDegree = 256) take the
+    # block-parallel argmin and the longest-first row schedule; everything
+    # still matches the oracle
     rng = np.random.default_rng(11)
     n = 6001
     u = [np.zeros(3000, np.int32), np.full(1500, 17, np.int32), rng.integers(0, n, 6000).astype(np.int32)]
@@ -460,8 +461,9 @@ def test_batched_walk_hub_rows_bitwise(n):
 
 
 def test_multi_segment_hub_successors_and_labels():
-    # rows longer than one 2048-neighbour segment are reduced segment-wise and
-    # combined; successors / centers / labels must equal the oracle's
+    # rows longer than one kHeavySegment (1024) segment are reduced
+    # segment-wise and combined; successors / centers / labels must equal the
+    # oracle's
     n = 9001
     rng = np.random.default_rng(99)
     u, v, _ = H.graphgen.random_edges(n, 3.0, unit=True, seed=99)
@@ -481,6 +483,88 @@ def test_multi_segment_hub_successors_and_labels():
         assert np.array_equal(succ[q], so)
         assert np.array_equal(res[q].center, co) and np.array_equal(res[q].cluster_index, cio)
         assert res[q].num_clusters == ko
+
+
+def test_heavy_row_boundary_degrees():
+    """Rows of degree exactly at and one past the GGD heavy-row threshold
+    (kHeavyDegree = 256) and at / past one and two heavy segments
+    (kHeavySegment = 1024), plus the batched-walk threshold (32): successors,
+    centers and labels equal the oracle's (ggd.cpp:7-57)."""
+    n = 12001
+    rng = np.random.default_rng(7)
+    degs = [31, 32, 33, 255, 256, 257, 1023, 1024, 1025, 2047, 2048, 2049, 3072, 3073]
+    hubs = np.arange(len(degs), dtype=np.int32) * 7 + 100
+    others = np.setdiff1d(np.arange(n, dtype=np.int32), hubs)
+    us, vs = [], []
+    bu = rng.choice(others, 30000).astype(np.int32)
+    bv = rng.choice(others, 30000).astype(np.int32)
+    us.append(bu)
+    vs.append(bv)
+    for h, d in zip(hubs, degs):
+        nb = rng.choice(others, size=d, replace=False).astype(np.int32)
+        us.append(np.full(d, h, np.int32))
+        vs.append(nb)
+    g = H.G(n, np.concatenate(us), np.concatenate(vs), None, 10.0)
+    assert list(np.diff(g.offsets)[hubs]) == degs
+    sig = [0.3, 1.0, 2.3, 5.0, 8.0, 12.0, 20.0, 30.0]
+    res, v_dev, succ = N.cluster_sweep(g.csr(N), sig, want_v=True, want_succ=True)
+    for q, s in enumerate(sig):
+        vo, so, co, cio, ko = O.cluster(g.offsets, g.nbr, g.wt, 10.0, s, workers=8)
+        assert_bits(v_dev[q], vo)
+        assert np.array_equal(succ[q], so)
+        assert np.array_equal(res[q].center, co) and np.array_equal(res[q].cluster_index, cio)
+        assert res[q].num_clusters == ko
+    # a field that makes every hub its neighbourhood's minimum / maximum
+    for vv in (np.arange(n, dtype=np.float64), -np.arange(n, dtype=np.float64)):
+        vv = vv.copy()
+        vv[hubs] = -1e9 if vv[0] == 0 else 1e9
+        assert np.array_equal(N.build_successors(g.csr(N), vv), O.build_successors(g.offsets, g.nbr, vv))
+
+
+def test_deep_monotone_chain_through_device_ggd():
+    """A 1M-node path whose field strictly decreases along it: the successor
+    map is ONE chain of depth n - 1 (0 -> 1 -> ... -> n-1, and reversed in the
+    second sigma column). The chase stops after its step bound and pointer
+    jumping finishes in <= ceil(log2 n) + 2 rounds (ggd.cpp:26-57); before
+    the bound, thread 0 alone walked n dependent loads."""
+    import time
+
+    import torch
+    n = 1 << 20
+    g = H.path(n)
+    dg = N.DeviceCsr(g.csr(N))
+    ar = torch.arange(n, dtype=torch.float64, device="cuda")
+    V = torch.stack([float(n) - ar, ar], dim=1).contiguous()  # node-major [n][2]
+    succ = torch.empty((2, n), dtype=torch.int32, device="cuda")
+    center, ci = torch.empty_like(succ), torch.empty_like(succ)
+    nc = torch.empty(2, dtype=torch.int32, device="cuda")
+    ws = torch.empty(N.dev_ggd_workspace(n, 2), dtype=torch.uint8, device="cuda")
+    for rep in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        N.dev_ggd(dg, V, 2, succ, center, ci, nc, ws)
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+    s = succ.cpu().numpy()
+    assert np.array_equal(s[0][:-1], np.arange(1, n)) and s[0][-1] == n - 1
+    assert np.array_equal(s[1][1:], np.arange(n - 1)) and s[1][0] == 0
+    c = center.cpu().numpy()
+    assert np.all(c[0] == n - 1) and np.all(c[1] == 0)
+    assert np.all(ci.cpu().numpy() == 0) and list(nc.cpu().numpy()) == [1, 1]
+    assert el < 0.5, f"deep chain took {el:.3f} s"
+
+
+def test_long_path_graph_sweep_properties():
+    """gqc_cluster_sweep on a 1M-node path (ties between equal-degree
+    interior nodes are broken by rounding noise, so chains of any depth can
+    form): GGD outputs satisfy ggd.cpp:7-57's properties over the whole graph."""
+    from tests.test_gpu_fullsize import check_ggd
+    n = 1 << 20
+    g = H.path(n)
+    sig = [0.5, 2.0, 5.0, 9.0, 14.0, 20.0, 25.0, 30.0]
+    res, v, succ = N.cluster_sweep(g.csr(N), sig, want_v=True, want_succ=True)
+    for q in range(len(sig)):
+        check_ggd(g.offsets, g.nbr, v[q], succ[q], res[q].center, res[q].cluster_index, res[q].num_clusters)
 
 
 @pytest.mark.parametrize("kernel,unit,mode", [(N.KERNEL_FASTFWD, False, N.EXP_EIGEN),

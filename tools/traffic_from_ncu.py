@@ -17,7 +17,8 @@ import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
-         "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+         "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3,
+         "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 FIELDS = {
     "dram_read": "dram__bytes_read.sum",
     "dram_write": "dram__bytes_write.sum",
@@ -28,6 +29,8 @@ FIELDS = {
     "fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "registers": "launch__registers_per_thread",
     "occupancy_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "dadd_per_cycle": "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum.per_cycle_elapsed",
+    "cycles_elapsed": "smsp__cycles_elapsed.avg",
 }
 
 
@@ -63,6 +66,8 @@ def main():
             except ValueError:
                 continue
             d[f] = v * SCALE.get(units[col[m]], 1.0)
+        if "dadd_per_cycle" in d and "cycles_elapsed" in d:  # fp64 adds executed (thread level)
+            d["dadd_thread_inst"] = d["dadd_per_cycle"] * d["cycles_elapsed"]
         if "dram_read" in d and "dram_write" in d:
             d["dram_bytes"] = d["dram_read"] + d["dram_write"]
         d["report"] = os.path.relpath(a.report, ROOT)
