@@ -285,8 +285,11 @@ def run_native(args):
     csr = N.Csr(off, nbr, None, W_DEFAULT)
     dg = N.DeviceCsr(csr, dev)
     stream = torch.cuda.Stream(dev)
-    block = sharded.row_block(n, world)
-    begin, end = sharded.row_shard(n, world, rank)
+    # cost-balanced row blocks (gqc_row_shards: degree + 4 per row), so a
+    # skewed graph (R-MAT's hubs sit at low ids) gives every rank equal work
+    bounds = [int(b) for b in N.row_shards(csr, world)]
+    block = max(bounds[r + 1] - bounds[r] for r in range(world))
+    begin, end = bounds[rank], bounds[rank + 1]
     rows = end - begin
 
     chunk = sharded.sigma_chunk(S, world)
@@ -308,7 +311,7 @@ def run_native(args):
         launches[0] += N.last_launch_count()
 
     with torch.cuda.stream(stream):
-        sweep = sharded.SigmaShardedSweep(n, S, rank, world, dev, pot_packed, ggd)
+        sweep = sharded.SigmaShardedSweep(n, S, rank, world, dev, pot_packed, ggd, bounds=bounds)
     shard = sweep.send  # this rank's rows, packed by sigma chunk
 
     def step(record=False):
@@ -448,7 +451,7 @@ def run_native(args):
                        "sigma_grid": f"log_sigma_grid(10, {S})", "kernel": args.kernel,
                        "distance": ("reference (graph.cpp:258-267, hop cap 1)" if args.hop_cap == 1 else
                                     f"k-hop extension, hop cap {args.hop_cap} (not a reference feature)"),
-                       "parallelism": f"potentials row-shard x{world}; all-to-all(V) by sigma chunk; "
+                       "parallelism": f"potentials row-shard x{world} (cost-balanced blocks); all-to-all(V) by sigma chunk; "
                                       f"GGD sigma-shard x{world}; "
                                       + ("all-gather(labels, counts)" if args.labels == "replicated"
                                          else "all-gather(counts), labels sharded by sigma"),
@@ -508,7 +511,9 @@ def e2e_leg(args, N, torch, dist, off, nbr, sig, rank, world, dev, stream, begin
         N.dev_ggd(dg, v_chunk, chunk, None, center, ci_out, nc_out, ws, stream)
 
     with torch.cuda.stream(stream):
-        sweep = sharded.SigmaShardedSweep(n, S, rank, world, dev, pot_packed, ggd)
+        sweep = sharded.SigmaShardedSweep(n, S, rank, world, dev, pot_packed, ggd,
+                                          bounds=[int(b) for b in N.row_shards(N.Csr(off, nbr, None, W_DEFAULT),
+                                                                                world)])
     s0, s1 = sweep.s_begin, sweep.s_end
     out_ci = torch.empty((max(s1 - s0, 1), n), dtype=torch.int32).pin_memory()
     out_nc = torch.empty(max(s1 - s0, 1), dtype=torch.int32).pin_memory()

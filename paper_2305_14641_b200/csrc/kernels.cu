@@ -374,25 +374,55 @@ __device__ __noinline__ void wait_slab(const int* flags, const int b1, const int
     __threadfence();
 }
 
-// Both chains of a W run of length L > 0 in the warp kernel (lane = sigma).
-// The common case — every lane's run ends inside the binade its chain has
-// cached, outside the tie binade — is one exact fma per chain and a warp vote;
-// only then the general ff_run walks the lanes that cross (binade crossings,
-// real adds, tie parity). Same result as ff_run2 bit for bit: with a valid
-// cache, flags == kJump and t < top, ff_run's first step is exactly s = t, and
-// otherwise ff_run runs from the unchanged state.
-__device__ __forceinline__ void ff_lean2(Chain& a, const double ca, Chain& b, const double cb, const int L) {
+// One chain's W run of length L > 0 when the one-fma fast path failed: the
+// run crosses the top of the cached binade (or the cache is one binade
+// behind after a neighbour add crossed it). A settled chain jumps the
+// provable in-binade steps, crosses with one real add, moves its cache to the
+// next binade incrementally (a settled crossing lands in [top, 2 top)) and
+// finishes the run there when it fits; anything else (several crossings,
+// real adds at c >= base/2, tie parity, a cold cache) takes ff_run.
+__device__ __forceinline__ void cross_run(Chain& ch, const double c, int L) {
+    if (ch.flags == kJump) {
+        if (!(ch.s < ch.top) && ch.s < ch.top + ch.top) {  // the cache is one binade behind
+            const double base = ch.top;
+            ch.top = __dadd_rn(base, base);
+            ch.inc = __dsub_rn(__dadd_rn(base, c), base);
+            ch.flags = kJump | (exp_field(base) == ch.f_tie ? kTie : 0);
+        } else if (ch.s < ch.top) {  // crossing inside the run
+            const double m = max_steps(ch, room_of(ch));
+            const double base = ch.top;
+            ch.s = __dadd_rn(__fma_rn(m, ch.inc, ch.s), c);
+            L -= static_cast<int>(m) + 1;
+            ch.top = __dadd_rn(base, base);
+            ch.inc = __dsub_rn(__dadd_rn(base, c), base);
+            ch.flags = kJump | (exp_field(base) == ch.f_tie ? kTie : 0);
+            if (L <= 0) return;
+        }
+        if (ch.flags == kJump) {
+            const double t = __fma_rn(static_cast<double>(L), ch.inc, ch.s);
+            if (t < ch.top) {
+                ch.s = t;
+                return;
+            }
+        }
+    }
+    ff_run(ch, c, L);
+}
+
+// Both chains of a W run of length L > 0 (lane = sigma): one exact fma per
+// chain when the run ends inside the cached binade (flags == kJump: jumpable,
+// not the tie binade); the lanes whose run crosses take cross_run. Same
+// result as ff_run2 bit for bit (every branch is a step of ff_run's loop).
+__device__ __forceinline__ void ff_event2(Chain& a, const double ca, Chain& b, const double cb, const int L) {
     const double Ld = static_cast<double>(L);
     const double ta = __fma_rn(Ld, a.inc, a.s);
     const double tb = __fma_rn(Ld, b.inc, b.s);
-    const bool oka = a.flags == kJump && ta < a.top;
-    const bool okb = b.flags == kJump && tb < b.top;
-    a.s = oka ? ta : a.s;
-    b.s = okb ? tb : b.s;
-    if (__any_sync(0xffffffffu, !(oka && okb))) {
-        if (!oka) ff_run(a, ca, L);
-        if (!okb) ff_run(b, cb, L);
-    }
+    const bool fa = a.flags == kJump && ta < a.top;
+    const bool fb = b.flags == kJump && tb < b.top;
+    if (fa) a.s = ta;
+    if (fb) b.s = tb;
+    if (!fa) cross_run(a, ca, L);
+    if (!fb) cross_run(b, cb, L);
 }
 
 // CSR neighbour load of the warp kernel. Under the polled upload the copy
@@ -494,7 +524,7 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
                 }
             } else {
 #if GQC_LEAN
-                if constexpr (kW == kUnit) ff_lean2(num, pW, den, eW, L);
+                if constexpr (kW == kUnit) ff_event2(num, pW, den, eW, L);
                 else ff_walk2(num, pW, den, eW, L);
 #elif GQC_WALK2
                 ff_walk2(num, pW, den, eW, L);

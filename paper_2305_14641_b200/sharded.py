@@ -131,7 +131,9 @@ class SigmaShardedSweep:
 
     Bytes on the wire per rank: (world-1)/world * n*S*8/world for V plus the
     labels gather, against (world-1)/world * n*S*(8+4) for all-gather(V) +
-    all-gather(succ); and no rank repeats another's GGD work.
+    all-gather(succ); and no rank repeats another's GGD work. Row blocks may
+    be uneven (cost-balanced `bounds`): the all-to-all then uses per-rank
+    split sizes and lands the chunk's rows in order.
 
       potentials_packed(begin, end, send, chunk, chunk_stride): V rows
           [begin, end) into the flat send buffer, sigma k of row i at
@@ -140,30 +142,43 @@ class SigmaShardedSweep:
     Padding (rows past n, sigmas past S) stays zero and is dropped.
     """
 
-    def __init__(self, n, n_sigma, rank, world, device, potentials_packed, ggd, group=None):
+    def __init__(self, n, n_sigma, rank, world, device, potentials_packed, ggd, group=None, bounds=None):
         self.n, self.S, self.rank, self.world, self.group = n, n_sigma, rank, world, group
-        self.block = row_block(n, world)
-        self.begin, self.end = row_shard(n, world, rank)
+        # row blocks: `bounds` (world + 1 ascending row ids, e.g. the
+        # cost-balanced gqc_row_shards, so skewed graphs give every rank the
+        # same work), else equal blocks of ceil(n / world)
+        if bounds is None:
+            bounds = [row_shard(n, world, r)[0] for r in range(world)] + [n]
+        self.bounds = [int(b) for b in bounds]
+        assert len(self.bounds) == world + 1 and self.bounds[0] == 0 and self.bounds[-1] == n
+        self.rows_of = [self.bounds[r + 1] - self.bounds[r] for r in range(world)]
+        self.begin, self.end = self.bounds[rank], self.bounds[rank + 1]
+        self.rows = self.end - self.begin
+        self.block = max(self.rows_of)
         self.chunk = sigma_chunk(n_sigma, world)
         self.s_begin, self.s_end = sigma_shard(n_sigma, world, rank)
         self.potentials_packed, self.ggd_op = potentials_packed, ggd
-        cells = world * self.block * self.chunk
-        self.send = torch.zeros(cells, dtype=torch.float64, device=device)
-        self.recv = torch.zeros(cells, dtype=torch.float64, device=device) if world > 1 else self.send
+        # send: this rank's rows, packed by sigma chunk ([world][rows][chunk]);
+        # recv: every rank's rows of this rank's chunk, in row order = the
+        # node-major [n][chunk] field (uneven all-to-all splits)
+        self.send = torch.zeros(max(1, world * self.rows * self.chunk), dtype=torch.float64, device=device)
+        self.recv = torch.zeros(n * self.chunk, dtype=torch.float64, device=device) if world > 1 else self.send
         self.ci = torch.zeros((self.chunk, n), dtype=torch.int32, device=device)
         self.nc = torch.zeros(self.chunk, dtype=torch.int32, device=device)
         self.ci_full = torch.empty((world * self.chunk, n), dtype=torch.int32, device=device) if world > 1 else self.ci
         self.nc_full = torch.empty(world * self.chunk, dtype=torch.int32, device=device) if world > 1 else self.nc
 
     def potentials(self):
-        if self.end > self.begin:
-            self.potentials_packed(self.begin, self.end, self.send, self.chunk, self.block * self.chunk)
+        if self.rows > 0:
+            self.potentials_packed(self.begin, self.end, self.send, self.chunk, self.rows * self.chunk)
 
     def exchange(self):
         """V of this rank's sigma chunk for all rows, node-major [n, chunk]."""
         if self.world > 1:
-            dist.all_to_all_single(self.recv, self.send, group=self.group)
-        return self.recv.view(self.world * self.block, self.chunk)[: self.n]
+            dist.all_to_all_single(self.recv, self.send[: self.world * self.rows * self.chunk],
+                                   output_split_sizes=[r * self.chunk for r in self.rows_of],
+                                   input_split_sizes=[self.rows * self.chunk] * self.world, group=self.group)
+        return self.recv[: self.n * self.chunk].view(self.n, self.chunk)
 
     def ggd(self, v_chunk):
         self.ggd_op(v_chunk, self.ci, self.nc)

@@ -124,7 +124,7 @@ def test_sigma_shards_partition_the_grid():
             assert all(b - a <= sharded.sigma_chunk(S, world) for a, b in got)
 
 
-def _worker_sigma(rank, world, port, result_path, n_nodes, sig):
+def _worker_sigma(rank, world, port, result_path, n_nodes, sig, bounds=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -148,7 +148,12 @@ def _worker_sigma(rank, world, port, result_path, n_nodes, sig):
                 ci[k] = torch.from_numpy(cik)
                 nc[k] = kk
 
-        sweep = sharded.SigmaShardedSweep(g.n, S, rank, world, "cpu", potentials_packed, ggd)
+        if bounds == "cost":  # gqc_row_shards (host-only call): degree-balanced blocks
+            from paper_2305_14641_b200 import native as N
+            b = [int(x) for x in N.row_shards(N.Csr(g.offsets, g.nbr, None, 10.0), world)]
+        else:
+            b = bounds
+        sweep = sharded.SigmaShardedSweep(g.n, S, rank, world, "cpu", potentials_packed, ggd, bounds=b)
         ci, nc = sweep.step()
         ok = tuple(ci.shape) == (S, g.n) and tuple(nc.shape) == (S,)
         ref = [O.cluster(g.offsets, g.nbr, g.wt, 10.0, s) for s in sig]
@@ -178,6 +183,21 @@ def test_gloo_sigma_sharded_ggd_matches_single_process(world, n_nodes, sig, tmp_
     # with the single-process labels of every sigma
     result = tmp_path / "r"
     mp.start_processes(_worker_sigma, args=(world, _free_port(), str(result), n_nodes, sig), nprocs=world,
+                       join=True, start_method="spawn")
+    for r in range(world):
+        assert (tmp_path / f"r.{r}").read_text() == "ok"
+
+
+@pytest.mark.parametrize("world,n_nodes,sig,bounds", [(2, 97, [0.7, 2.3, 5.0, 30.0], "cost"),
+                                                      (3, 101, [0.7, 2.3, 5.0, 9.0, 30.0], "cost"),
+                                                      (2, 97, [0.7, 2.3, 30.0], [0, 11, 97]),
+                                                      (3, 80, [1.0, 4.0, 9.0], [0, 0, 70, 80])])  # an empty rank
+def test_gloo_sigma_sharded_uneven_row_blocks(world, n_nodes, sig, bounds, tmp_path):
+    # cost-balanced (gqc_row_shards) or arbitrary uneven row blocks: the
+    # all-to-all with per-rank split sizes still lands every chunk's rows in
+    # order, and every rank ends with the single-process labels
+    result = tmp_path / "r"
+    mp.start_processes(_worker_sigma, args=(world, _free_port(), str(result), n_nodes, sig, bounds), nprocs=world,
                        join=True, start_method="spawn")
     for r in range(world):
         assert (tmp_path / f"r.{r}").read_text() == "ok"
