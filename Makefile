@@ -11,7 +11,7 @@ ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xptxas -v \
              -Xcompiler -fPIC,-O2,-ffp-contract=off,-Wall -I include -I $(CSRC)
 LIBGQC    := $(PKG)/libgqc.so
-GQC_SRCS  := $(CSRC)/capi.cu $(CSRC)/kernels.cu $(CSRC)/khop.cu $(CSRC)/host_exp.cpp
+GQC_SRCS  := $(CSRC)/capi.cu $(CSRC)/kernels.cu $(CSRC)/khop.cu $(CSRC)/csr_build.cu $(CSRC)/host_exp.cpp
 GQC_HDRS  := include/gqc.h $(CSRC)/gqc_internal.h $(CSRC)/ff_chain.cuh
 
 all: $(LIBGQC) oracle facade

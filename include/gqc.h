@@ -150,6 +150,27 @@ gqc_status gqc_cluster_sweep_intra(const gqc_csr* g, const double* sigmas, int32
                                    int32_t* succ_out, int32_t* center_out, int32_t* cluster_index_out,
                                    int32_t* num_clusters_out, int64_t* intra_out);
 
+/* ------------------------------------------------------------- ingestion */
+/* One input edge, laid out like graphqc::Edge (graph.hpp:20-24). */
+typedef struct gqc_edge {
+    int32_t u, v;
+    double w;
+} gqc_edge;
+
+/* The CSR of graphqc::Graph(n, edges, W) (graph.cpp:25-71), built on the
+ * device by two radix sorts: validation in input order (the first edge with
+ * an endpoint outside [0, n) -> GQC_ERANGE "edge endpoint out of range", or
+ * with weight <= 0 -> GQC_EINVAL "edge weight must be positive"), self loops
+ * dropped, duplicate undirected pairs keep their first occurrence, rows
+ * ascending. Host outputs: offsets[n+1]; nbr and w_out (optional) with room
+ * for 2*m entries; *nnz_out; *unit_out = 1 when every kept weight is 1.0.
+ * Dropped duplicates whose weight differs from the kept one (the reference
+ * warns about each, in input order): dup_out[2j] = dropped input index,
+ * dup_out[2j+1] = kept input index, ascending by dropped index, at most
+ * dup_cap pairs; *n_dup_out = how many exist. m < 2^32. */
+gqc_status gqc_build_csr(int32_t n, int64_t m, const gqc_edge* edges, int64_t* offsets, int32_t* nbr, double* w_out,
+                         int64_t* nnz_out, int32_t* unit_out, int64_t* dup_out, int64_t dup_cap, int64_t* n_dup_out);
+
 /* -------------------------------------------------------- multi-device API */
 /* The row-sharded sweep of one process over several GPUs — the reference's
  * compute_potentials_parallel(g, sigma, workers) (potential.cpp:62-87) with

@@ -1235,6 +1235,40 @@ gqc_status gqc_potentials_multi(const gqc_csr* g, const double* sigmas, int32_t 
     });
 }
 
+gqc_status gqc_build_csr(int32_t n, int64_t m, const gqc_edge* edges, int64_t* offsets, int32_t* nbr, double* w_out,
+                         int64_t* nnz_out, int32_t* unit_out, int64_t* dup_out, int64_t dup_cap, int64_t* n_dup_out) {
+    static_assert(sizeof(gqc_edge) == sizeof(GqcEdge), "edge layout");
+    return guarded([&] {
+        if (n < 1) fail(GQC_EINVAL, "graph needs at least one node");  // graph.cpp:28
+        if (m < 0 || m >= (1ll << 32)) fail(GQC_EINVAL, "edge count out of range");
+        if (!offsets || !nnz_out || (m > 0 && (!edges || !nbr))) fail(GQC_EINVAL, "null buffer");
+        DeviceCtx& C = ctx();
+        long long nnz = 0, first = -1;
+        int unit = 1;
+        std::vector<long long> conf;
+        cuda_check(build_csr_device(n, m, reinterpret_cast<const GqcEdge*>(edges), offsets, nbr, w_out, &nnz,
+                                    n_dup_out ? &conf : nullptr, &unit, &first, C.pool, C.stream),
+                   "CSR build");
+        if (first >= 0) {  // graph.cpp:33-39: the first offending edge, endpoint before weight
+            if (first & 1) fail(GQC_EINVAL, "edge weight must be positive");
+            fail(GQC_ERANGE, "edge endpoint out of range");
+        }
+        *nnz_out = nnz;
+        if (unit_out) *unit_out = unit;
+        if (n_dup_out) {
+            if (!conf.empty() && conf.back() == -1) fail(GQC_ENOMEM, "too many conflicting duplicate edges");
+            std::vector<std::pair<long long, long long>> pairs(conf.size() / 2);
+            for (std::size_t j = 0; j < pairs.size(); ++j) pairs[j] = {conf[2 * j], conf[2 * j + 1]};
+            std::sort(pairs.begin(), pairs.end());
+            *n_dup_out = static_cast<int64_t>(pairs.size());
+            for (std::size_t j = 0; j < pairs.size() && static_cast<int64_t>(j) < dup_cap; ++j) {
+                dup_out[2 * j] = pairs[j].first;
+                dup_out[2 * j + 1] = pairs[j].second;
+            }
+        }
+    });
+}
+
 gqc_status gqc_row_shards(const gqc_csr* g, int32_t n_shards, int32_t* bounds) {
     return guarded([&] {
         check_csr_shape(g);

@@ -3,6 +3,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 namespace gqc {
 
@@ -144,6 +145,20 @@ struct KhopTable {
 };
 void fill_khop_table(KhopTable& t, int s, double sigma, int hop_cap, int exp_mode);
 int launch_potentials_khop(const PotentialLaunch& p, int hop_cap, const KhopTable& t, void* pool, void* stream);
+
+// Edge-list ingestion on the device (csr_build.cu): graphqc::Graph's CSR
+// (graph.cpp:25-71) from m input edges. offsets[n+1], nbr / w_out (capacity
+// >= 2m, w_out optional) are host outputs; conflicts (optional) receives
+// (dropped, kept) input-index pairs of duplicates with a different weight
+// (unsorted; a trailing -1 marks an overflow); *first_error = -1 or
+// k << 1 | kind of the first offending edge (0 endpoint, 1 weight).
+struct GqcEdge {
+    std::int32_t u, v;
+    double w;
+};
+int build_csr_device(int n, long long m, const GqcEdge* host_edges, std::int64_t* offsets, std::int32_t* nbr,
+                     double* w_out, long long* nnz_out, std::vector<long long>* conflicts, int* unit_out,
+                     long long* first_error, void* pool, void* stream);
 
 // SM count of the calling thread's current device (cached per device).
 int sm_count();

@@ -38,13 +38,7 @@
 #ifndef GQC_WALK2
 #define GQC_WALK2 1
 #endif
-// GQC_LEAN=1: W runs of the warp kernel (unit weights) take a vote-guarded
-// fast path — one exact fma per chain when every lane's run stays inside
-// its cached binade — and fall back to the general ff_run only for the lanes
-// that cross (see ff_lean2).
-#ifndef GQC_LEAN
-#define GQC_LEAN 1
-#endif
+
 #ifndef GQC_LANE_OUT_SMEM
 #define GQC_LANE_OUT_SMEM 1
 #endif
@@ -374,57 +368,6 @@ __device__ __noinline__ void wait_slab(const int* flags, const int b1, const int
     __threadfence();
 }
 
-// One chain's W run of length L > 0 when the one-fma fast path failed: the
-// run crosses the top of the cached binade (or the cache is one binade
-// behind after a neighbour add crossed it). A settled chain jumps the
-// provable in-binade steps, crosses with one real add, moves its cache to the
-// next binade incrementally (a settled crossing lands in [top, 2 top)) and
-// finishes the run there when it fits; anything else (several crossings,
-// real adds at c >= base/2, tie parity, a cold cache) takes ff_run.
-__device__ __forceinline__ void cross_run(Chain& ch, const double c, int L) {
-    if (ch.flags == kJump) {
-        if (!(ch.s < ch.top) && ch.s < ch.top + ch.top) {  // the cache is one binade behind
-            const double base = ch.top;
-            ch.top = __dadd_rn(base, base);
-            ch.inc = __dsub_rn(__dadd_rn(base, c), base);
-            ch.flags = kJump | (exp_field(base) == ch.f_tie ? kTie : 0);
-        } else if (ch.s < ch.top) {  // crossing inside the run
-            const double m = max_steps(ch, room_of(ch));
-            const double base = ch.top;
-            ch.s = __dadd_rn(__fma_rn(m, ch.inc, ch.s), c);
-            L -= static_cast<int>(m) + 1;
-            ch.top = __dadd_rn(base, base);
-            ch.inc = __dsub_rn(__dadd_rn(base, c), base);
-            ch.flags = kJump | (exp_field(base) == ch.f_tie ? kTie : 0);
-            if (L <= 0) return;
-        }
-        if (ch.flags == kJump) {
-            const double t = __fma_rn(static_cast<double>(L), ch.inc, ch.s);
-            if (t < ch.top) {
-                ch.s = t;
-                return;
-            }
-        }
-    }
-    ff_run(ch, c, L);
-}
-
-// Both chains of a W run of length L > 0 (lane = sigma): one exact fma per
-// chain when the run ends inside the cached binade (flags == kJump: jumpable,
-// not the tie binade); the lanes whose run crosses take cross_run. Same
-// result as ff_run2 bit for bit (every branch is a step of ff_run's loop).
-__device__ __forceinline__ void ff_event2(Chain& a, const double ca, Chain& b, const double cb, const int L) {
-    const double Ld = static_cast<double>(L);
-    const double ta = __fma_rn(Ld, a.inc, a.s);
-    const double tb = __fma_rn(Ld, b.inc, b.s);
-    const bool fa = a.flags == kJump && ta < a.top;
-    const bool fb = b.flags == kJump && tb < b.top;
-    if (fa) a.s = ta;
-    if (fb) b.s = tb;
-    if (!fa) cross_run(a, ca, L);
-    if (!fb) cross_run(b, cb, L);
-}
-
 // CSR neighbour load of the warp kernel. Under the polled upload the copy
 // engine is still writing nbr while the kernel runs, so those loads are
 // coherent (ld.relaxed.gpu, ordered after the slab flag's acquire) instead of
@@ -523,10 +466,7 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
                     ch.top = 0.0;
                 }
             } else {
-#if GQC_LEAN
-                if constexpr (kW == kUnit) ff_event2(num, pW, den, eW, L);
-                else ff_walk2(num, pW, den, eW, L);
-#elif GQC_WALK2
+#if GQC_WALK2
                 ff_walk2(num, pW, den, eW, L);
 #else
                 ff_run2(num, pW, den, eW, L);

@@ -83,6 +83,7 @@ def _load():
         "gqc_cluster_sweep_multi": [P, P, i32, P, i32, P, P, P, P, P, P],
         "gqc_potentials_multi": [P, P, i32, P, i32, P],
         "gqc_row_shards": [P, i32, P],
+        "gqc_build_csr": [i32, i64, P, P, P, P, P, P, P, i64, P],
         "gqc_dev_potentials": [P, P, i32, i32, i32, P, P],
         "gqc_dev_potentials_packed": [P, P, i32, i32, i32, P, i32, i64, P],
         "gqc_dev_ggd": [P, P, i32, P, P, P, P, P, C.c_size_t, P],
@@ -320,6 +321,26 @@ def cluster_sweep(g: Csr, sigmas: Sequence[float], want_v: bool = False, want_su
     else:
         out = [ClusterAssignment(center[q], ci[q], int(k[q])) for q in range(S)]
     return out, v, succ
+
+
+def build_csr(n: int, u, v, w=None, dup_cap: int = 1 << 16):
+    """gqc_build_csr: graphqc::Graph's CSR (graph.cpp:25-71) from an edge list
+    in input order, on the device. Returns (offsets, nbr, weights, unit,
+    dups) with dups = [(dropped, kept)] input indices of conflicting duplicates."""
+    m = len(u)
+    e = np.zeros(m, dtype=[("u", np.int32), ("v", np.int32), ("w", np.float64)])
+    e["u"], e["v"] = u, v
+    e["w"] = 1.0 if w is None else w
+    off = np.zeros(n + 1, dtype=np.int64)
+    nbr = np.zeros(max(1, 2 * m), dtype=np.int32)
+    wt = np.zeros(max(1, 2 * m), dtype=np.float64)
+    nnz, unit, nd = np.zeros(1, np.int64), np.zeros(1, np.int32), np.zeros(1, np.int64)
+    dup = np.zeros(2 * dup_cap, dtype=np.int64)
+    _check(_lib.gqc_build_csr(int(n), m, _ptr(e), _ptr(off), _ptr(nbr), _ptr(wt), _ptr(nnz), _ptr(unit), _ptr(dup),
+                              dup_cap, _ptr(nd)))
+    k = int(nnz[0])
+    d = int(min(nd[0], dup_cap))
+    return off, nbr[:k], wt[:k], bool(unit[0]), [(int(dup[2 * j]), int(dup[2 * j + 1])) for j in range(d)]
 
 
 def row_shards(g: Csr, n_shards: int) -> np.ndarray:
