@@ -659,6 +659,10 @@ struct SuccOut {
 #define GQC_HEAVY_UNROLL 4
 #endif
 constexpr int kSuccUnroll = GQC_SUCC_UNROLL;    // gathers in flight per thread (light rows)
+#ifndef GQC_SUCC_SUB
+#define GQC_SUCC_SUB 8
+#endif
+constexpr int kSuccSub = GQC_SUCC_SUB;  // sigmas per light-row argmin launch (L2-resident V slice)
 constexpr int kHeavyUnroll = GQC_HEAVY_UNROLL;  // gathers in flight per warp (heavy rows)
 
 __device__ __forceinline__ bool lex_less(double va, int ia, double vb, int ib) {
@@ -1469,23 +1473,34 @@ int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nb
         const SuccOut O{out + c0 * out_col, out_row, out_col};
         // light rows: the kernels index threads in 32 bits, so the row range
         // goes in sub-launches of fewer than 2^31 threads (graphs of ~67M+
-        // nodes at 32 sigmas), each with its output moved to its first row
+        // nodes at 32 sigmas), each with its output moved to its first row.
+        // The plain argmin runs kSuccSub sigmas per launch over all rows: the
+        // gathers of one launch touch only that slice of every node's V line
+        // (kSuccSub * 8 B of N nodes: 64 MB at LFR 1M), which stays in L2
+        // across the launch instead of the whole field (256 MB > L2).
         const long long per = ((1ll << 31) - 2 * kBlock) / 32;
         for (long long r0 = 0; r0 < rows; r0 += per) {
             const int rr = static_cast<int>(std::min<long long>(per, rows - r0));
-            const SuccOut Or{O.out + r0 * out_row, out_row, out_col};
             const int rb = row_begin + static_cast<int>(r0);
-            if (co && co->dir)
+            if (co && co->dir) {
+                const SuccOut Or{O.out + r0 * out_row, out_row, out_col};
                 successors_class_kernel<<<grid_for(static_cast<long long>(rr) * 32), kBlock, 0, st>>>(
                     off, nbr, v, ld, s0 + c0, Sc, rb, rr, Or, *co);
-            else
-                successors_kernel<<<grid_for(static_cast<long long>(rr) * Sc), kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0,
-                                                                                              Sc, rb, rr, Or);
+                count_launch();
+            } else {
+                for (int q0 = 0; q0 < Sc; q0 += kSuccSub) {
+                    const int Sq = std::min(kSuccSub, Sc - q0);
+                    const SuccOut Or{O.out + r0 * out_row + q0 * out_col, out_row, out_col};
+                    successors_kernel<<<grid_for(static_cast<long long>(rr) * Sq), kBlock, 0, st>>>(
+                        off, nbr, v, ld, s0 + c0 + q0, Sq, rb, rr, Or);
+                    count_launch();
+                }
+            }
         }
         successors_heavy_kernel<<<num_sms * 8, kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, items, counts,
                                                                  part_v, part_i, O);
         successors_combine_kernel<<<num_sms * 2, kBlock, 0, st>>>(multi, counts, part_v, part_i, Sc, row_begin, O);
-        count_launch(3);
+        count_launch(2);
     }
     cudaFreeAsync(scratch, st);
     return cudaGetLastError();
