@@ -111,6 +111,11 @@ int32_t gqc_device_count(void);
  * (the reference has no device); the CLI uses it to overlap CUDA start-up
  * (~0.5-1.5 s per process) with edge-list parsing. */
 gqc_status gqc_init(void);
+/* 1 once this process has created the context of GQC_OPT_DEVICE (gqc_init or
+ * any call on it), else 0. Never blocks or initializes anything: a host
+ * program can pick a device path only when it costs no start-up (the facade's
+ * edge-list loader builds the CSR on the device when it is ready). */
+int32_t gqc_device_ready(void);
 
 /* ---------------------------------------------------------------- host API */
 

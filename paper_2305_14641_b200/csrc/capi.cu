@@ -249,6 +249,8 @@ int visible_devices() {
     return count;
 }
 
+std::atomic<int> g_ready[64];  // device contexts fully created (gqc_device_ready)
+
 // The context of device `dev`, locked by this call (see t_held) and created
 // on first use; the calling thread is bound to the device.
 DeviceCtx& ctx_of(int dev) {
@@ -282,6 +284,7 @@ DeviceCtx& ctx_of(int dev) {
         std::uint64_t keep = ~0ull;
         cuda_check(cudaMemPoolSetAttribute(c.pool, cudaMemPoolAttrReleaseThreshold, &keep), "cudaMemPoolSetAttribute");
     }
+    if (dev >= 0 && dev < 64) g_ready[dev].store(1);
     return c;
 }
 
@@ -583,6 +586,11 @@ extern "C" {
 const char* gqc_last_error(void) { return t_err.c_str(); }
 const char* gqc_version(void) { return "gqc 0.1 sm_100a"; }
 int64_t gqc_last_launch_count(void) { return t_launches; }
+
+int32_t gqc_device_ready(void) {
+    const int d = g_opt.device.load();
+    return d >= 0 && d < 64 ? g_ready[d].load() : 0;
+}
 
 int32_t gqc_device_count(void) {
     int c = 0;

@@ -307,75 +307,115 @@ GQC_HD inline void ff_walk2(Chain& a, const double ca, Chain& b, const double cb
 #ifndef GQC_WALK_COUNT
 #define GQC_WALK_COUNT()
 #endif
+// One accumulator's position in a batched walk: sum s, next event e, first
+// column not yet added pos.
+struct WalkState {
+    double s;
+    int e, pos;
+};
+
+// One iteration of the batched walk: everything up to the next binade
+// crossing (or the range's end) plus that crossing event.
+template <class Cols>
+GQC_HD inline void walk_step(WalkState& w, const double c, const double c1, const int tie_c, const int tie_c1,
+                             const Cols& col, const int end) {
+    GQC_WALK_COUNT();
+    double s = w.s;
+    int e = w.e, pos = w.pos;
+    const int f = gqc_max(exp_field(s), 1);
+    const double base = pow2_field(f);
+    const double top = gqc_add(base, base);
+    const double half = gqc_mul(base, 0.5);
+    if (c < half && c1 < half && f != tie_c && f != tie_c1) {
+        const double inc = gqc_sub(gqc_add(base, c), base);
+        const double inc1 = gqc_sub(gqc_add(base, c1), base);
+        int lo = e - 1, hi = end - 1;  // last event whose sum stays below top (e - 1: none)
+        {  // common case: the rest of the range stays in the binade
+            const double t = gqc_fma(static_cast<double>(end - e), inc1,
+                                     gqc_fma(static_cast<double>(col(end - 1) - pos - (end - 1 - e)), inc, s));
+            if (t < top) lo = hi;
+        }
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            const double t = gqc_fma(static_cast<double>(mid - e + 1), inc1,
+                                     gqc_fma(static_cast<double>(col(mid) - pos - (mid - e)), inc, s));
+            if (t < top) lo = mid;
+            else hi = mid - 1;
+        }
+        if (lo >= e) {
+            const int cl = col(lo);
+            s = gqc_fma(static_cast<double>(lo - e + 1), inc1,
+                        gqc_fma(static_cast<double>(cl - pos - (lo - e)), inc, s));
+            pos = cl + 1;
+            e = lo + 1;
+            if (e == end) {
+                w.s = s;
+                w.e = e;
+                w.pos = pos;
+                return;
+            }
+        }
+        // event e leaves the binade: inside its W run or at its neighbour add
+        const int ce = col(e);
+        const int L = ce - pos;
+        const double t = gqc_fma(static_cast<double>(L), inc, s);
+        if (t < top) {
+            s = t;
+        } else {
+            Chain ch;
+            ch.s = s;
+            ch.top = top;
+            ch.inc = inc;
+            ch.f_tie = tie_c;
+            ch.flags = kJump;
+            const double m = max_steps(ch, room_of(ch));
+            ch.s = gqc_add(gqc_fma(m, inc, s), c);
+            ch.top = 0.0;
+            ff_run(ch, c, L - static_cast<int>(m) - 1);
+            s = ch.s;
+        }
+        s = gqc_add(s, c1);
+        pos = ce + 1;
+        ++e;
+    } else {  // one event at a time (tiny sums, tie binades)
+        const int ce = col(e);
+        if (ce > pos) {
+            Chain ch = make_chain(s, c);
+            ch.f_tie = tie_c;
+            ff_run(ch, c, ce - pos);
+            s = ch.s;
+        }
+        s = gqc_add(s, c1);
+        pos = ce + 1;
+        ++e;
+    }
+    w.s = s;
+    w.e = e;
+    w.pos = pos;
+}
+
 template <class Cols>
 GQC_HD inline double walk_events(double s, const double c, const double c1, const int tie_c, const int tie_c1,
                                  const Cols& col, int e, const int end, int pos) {
-    while (e < end) {
-        GQC_WALK_COUNT();
-        const int f = gqc_max(exp_field(s), 1);
-        const double base = pow2_field(f);
-        const double top = gqc_add(base, base);
-        const double half = gqc_mul(base, 0.5);
-        if (c < half && c1 < half && f != tie_c && f != tie_c1) {
-            const double inc = gqc_sub(gqc_add(base, c), base);
-            const double inc1 = gqc_sub(gqc_add(base, c1), base);
-            int lo = e - 1, hi = end - 1;  // last event whose sum stays below top (e - 1: none)
-            {  // common case: the rest of the range stays in the binade
-                const double t = gqc_fma(static_cast<double>(end - e), inc1,
-                                         gqc_fma(static_cast<double>(col(end - 1) - pos - (end - 1 - e)), inc, s));
-                if (t < top) lo = hi;
-            }
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                const double t = gqc_fma(static_cast<double>(mid - e + 1), inc1,
-                                         gqc_fma(static_cast<double>(col(mid) - pos - (mid - e)), inc, s));
-                if (t < top) lo = mid;
-                else hi = mid - 1;
-            }
-            if (lo >= e) {
-                const int cl = col(lo);
-                s = gqc_fma(static_cast<double>(lo - e + 1), inc1,
-                            gqc_fma(static_cast<double>(cl - pos - (lo - e)), inc, s));
-                pos = cl + 1;
-                e = lo + 1;
-                if (e == end) break;
-            }
-            // event e leaves the binade: inside its W run or at its neighbour add
-            const int ce = col(e);
-            const int L = ce - pos;
-            const double t = gqc_fma(static_cast<double>(L), inc, s);
-            if (t < top) {
-                s = t;
-            } else {
-                Chain ch;
-                ch.s = s;
-                ch.top = top;
-                ch.inc = inc;
-                ch.f_tie = tie_c;
-                ch.flags = kJump;
-                const double m = max_steps(ch, room_of(ch));
-                ch.s = gqc_add(gqc_fma(m, inc, s), c);
-                ch.top = 0.0;
-                ff_run(ch, c, L - static_cast<int>(m) - 1);
-                s = ch.s;
-            }
-            s = gqc_add(s, c1);
-            pos = ce + 1;
-            ++e;
-        } else {  // one event at a time (tiny sums, tie binades)
-            const int ce = col(e);
-            if (ce > pos) {
-                Chain ch = make_chain(s, c);
-                ch.f_tie = tie_c;
-                ff_run(ch, c, ce - pos);
-                s = ch.s;
-            }
-            s = gqc_add(s, c1);
-            pos = ce + 1;
-            ++e;
-        }
+    WalkState w{s, e, pos};
+    while (w.e < end) walk_step(w, c, c1, tie_c, tie_c1, col, end);
+    return w.s;
+}
+
+// Both accumulators of a row over events [e, end) in one loop: the warp
+// iterates max(crossings) times over the two chains instead of the sum of
+// two walks, and the two dependency chains interleave.
+template <class Cols>
+GQC_HD inline void walk_events2(double& sa, const double ca, const double c1a, const int ta, const int t1a, double& sb,
+                                const double cb, const double c1b, const int tb, const int t1b, const Cols& col,
+                                const int e, const int end, const int pos) {
+    WalkState a{sa, e, pos}, b{sb, e, pos};
+    while (a.e < end || b.e < end) {
+        if (a.e < end) walk_step(a, ca, c1a, ta, t1a, col, end);
+        if (b.e < end) walk_step(b, cb, c1b, tb, t1b, col, end);
     }
-    return s;
+    sa = a.s;
+    sb = b.s;
 }
 
 // ---------------------------------------------------------------------------

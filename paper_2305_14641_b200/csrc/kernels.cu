@@ -38,6 +38,10 @@
 #ifndef GQC_WALK2
 #define GQC_WALK2 1
 #endif
+// GQC_WALK_EVENTS2=1: the batched walk advances both accumulators in one loop
+#ifndef GQC_WALK_EVENTS2
+#define GQC_WALK_EVENTS2 1
+#endif
 
 #ifndef GQC_LANE_OUT_SMEM
 #define GQC_LANE_OUT_SMEM 1
@@ -203,9 +207,16 @@ __device__ __forceinline__ void first_run(Chain& ch, const double c, const Prefi
 // (neighbours and the row itself); K2 takes the first run from the prefix
 // table and every later run through the two-chain fast-forward.
 // ---------------------------------------------------------------------------
+// Thread-per-(row, sigma) launches of at least this many rows take their rows
+// in descending-degree order (order[r] = row of slot r).
+#ifndef GQC_SORT_ROWS_MIN
+#define GQC_SORT_ROWS_MIN 4096
+#endif
+constexpr int kSortRowsMin = GQC_SORT_ROWS_MIN;
+
 template <bool kFF, int kW>
 __global__ void __launch_bounds__(kBlock) potential_kernel(const __grid_constant__ PotentialLaunch P,
-                                                           const PrefixTable T) {
+                                                           const PrefixTable T, const int* __restrict__ order) {
     __shared__ double sc[kSigmaFields][kMaxSigmaPerLaunch];
     for (int idx = threadIdx.x; idx < kSigmaFields * kMaxSigmaPerLaunch; idx += blockDim.x) {
         const int ss = idx % kMaxSigmaPerLaunch, f = idx / kMaxSigmaPerLaunch;
@@ -216,9 +227,9 @@ __global__ void __launch_bounds__(kBlock) potential_kernel(const __grid_constant
     const int S = P.n_sigma;
     const long long tid = static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x;
     const int s = static_cast<int>(tid % S);
-    const long long r64 = P.row_begin + tid / S;
-    if (r64 >= P.row_end) return;
-    const int i = static_cast<int>(r64);
+    const long long r64 = tid / S;
+    if (r64 >= P.row_end - P.row_begin) return;
+    const int i = order ? __ldg(order + r64) : P.row_begin + static_cast<int>(r64);
 
     const double e1 = sc[4][s], p1 = sc[5][s];
     const int n = P.n;
@@ -562,8 +573,12 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
             } colf{cols};
             const int tie_p1 = tie_binade(p1), tie_e1 = tie_binade(e1);
             auto walk = [&](const int j0, const int j1) {
+#if GQC_WALK_EVENTS2
+                walk_events2(num.s, pW, p1, tie_num, tie_p1, den.s, eW, e1, tie_den, tie_e1, colf, j0, j1, pos);
+#else
                 num.s = walk_events(num.s, pW, p1, tie_num, tie_p1, colf, j0, j1, pos);
                 den.s = walk_events(den.s, eW, e1, tie_den, tie_e1, colf, j0, j1, pos);
+#endif
                 num.top = 0.0;  // the chains' binade caches are stale now
                 den.top = 0.0;
                 pos = cols[j1 - 1] + 1;
@@ -660,7 +675,7 @@ struct SuccOut {
 #endif
 constexpr int kSuccUnroll = GQC_SUCC_UNROLL;    // gathers in flight per thread (light rows)
 #ifndef GQC_SUCC_SUB
-#define GQC_SUCC_SUB 8
+#define GQC_SUCC_SUB 32
 #endif
 constexpr int kSuccSub = GQC_SUCC_SUB;  // sigmas per light-row argmin launch (L2-resident V slice)
 constexpr int kHeavyUnroll = GQC_HEAVY_UNROLL;  // gathers in flight per warp (heavy rows)
@@ -1217,20 +1232,55 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
         }
         cudaFreeAsync(sched, st);
     } else {
+        // thread per (row, sigma): rows in descending-degree order, so the
+        // lanes of a warp walk rows with the same number of events (one sort
+        // per launch; small launches keep the natural order)
+        const int rows = p.row_end - p.row_begin;
+        const int* order = nullptr;
+        void* sched = nullptr;
+        if (rows >= kSortRowsMin) {
+            std::size_t sort_bytes = 0;
+            cub::DeviceRadixSort::SortPairsDescending(nullptr, sort_bytes, static_cast<const int*>(nullptr),
+                                                      static_cast<int*>(nullptr), static_cast<const int*>(nullptr),
+                                                      static_cast<int*>(nullptr), rows);
+            const std::size_t arr = ((static_cast<std::size_t>(rows) * sizeof(int)) + 255) & ~static_cast<std::size_t>(255);
+            cudaError_t e = cudaMallocFromPoolAsync(&sched, 4 * arr + sort_bytes, static_cast<cudaMemPool_t>(pool), st);
+            if (e != cudaSuccess) {
+                if (mem) cudaFreeAsync(mem, st);
+                return e;
+            }
+            char* b = static_cast<char*>(sched);
+            int* deg_in = reinterpret_cast<int*>(b);
+            int* deg_out = reinterpret_cast<int*>(b + arr);
+            int* id_in = reinterpret_cast<int*>(b + 2 * arr);
+            int* id_out = reinterpret_cast<int*>(b + 3 * arr);
+            row_degree_kernel<<<grid_for(rows), kBlock, 0, st>>>(reinterpret_cast<const long long*>(p.offsets),
+                                                                  p.row_begin, rows, deg_in, id_in, nullptr, 0, 0, 0);
+            e = cub::DeviceRadixSort::SortPairsDescending(b + 4 * arr, sort_bytes, deg_in, deg_out, id_in, id_out, rows,
+                                                          0, 32, st);
+            count_launch(3);
+            if (e != cudaSuccess) {
+                cudaFreeAsync(sched, st);
+                if (mem) cudaFreeAsync(mem, st);
+                return e;
+            }
+            order = id_out;
+        }
         switch (p.weight_mode) {
             case kUnit:
-                if (ff) potential_kernel<true, kUnit><<<grid, kBlock, 0, st>>>(p, T);
-                else potential_kernel<false, kUnit><<<grid, kBlock, 0, st>>>(p, T);
+                if (ff) potential_kernel<true, kUnit><<<grid, kBlock, 0, st>>>(p, T, order);
+                else potential_kernel<false, kUnit><<<grid, kBlock, 0, st>>>(p, T, order);
                 break;
             case kDevicePexp:
-                if (ff) potential_kernel<true, kDevicePexp><<<grid, kBlock, 0, st>>>(p, T);
-                else potential_kernel<false, kDevicePexp><<<grid, kBlock, 0, st>>>(p, T);
+                if (ff) potential_kernel<true, kDevicePexp><<<grid, kBlock, 0, st>>>(p, T, order);
+                else potential_kernel<false, kDevicePexp><<<grid, kBlock, 0, st>>>(p, T, order);
                 break;
             default:
-                if (ff) potential_kernel<true, kEntryTable><<<grid, kBlock, 0, st>>>(p, T);
-                else potential_kernel<false, kEntryTable><<<grid, kBlock, 0, st>>>(p, T);
+                if (ff) potential_kernel<true, kEntryTable><<<grid, kBlock, 0, st>>>(p, T, order);
+                else potential_kernel<false, kEntryTable><<<grid, kBlock, 0, st>>>(p, T, order);
                 break;
         }
+        if (sched) cudaFreeAsync(sched, st);
     }
     count_launch();
     cudaError_t e = cudaGetLastError();
@@ -1474,10 +1524,12 @@ int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nb
         // light rows: the kernels index threads in 32 bits, so the row range
         // goes in sub-launches of fewer than 2^31 threads (graphs of ~67M+
         // nodes at 32 sigmas), each with its output moved to its first row.
-        // The plain argmin runs kSuccSub sigmas per launch over all rows: the
-        // gathers of one launch touch only that slice of every node's V line
-        // (kSuccSub * 8 B of N nodes: 64 MB at LFR 1M), which stays in L2
-        // across the launch instead of the whole field (256 MB > L2).
+        // GQC_SUCC_SUB < 32 runs the plain argmin in launches of that many
+        // sigmas over all rows, so each launch gathers one slice of every
+        // node's V line (8 sigmas: 64 MB at LFR 1M, L2-sized). Measured (32
+        // sigmas, GGD ms, 32 / 8 / 4 per launch): LFR 1M 1.33 / 1.87 / 2.58,
+        // R-MAT 22 6.06 / 5.00 / 6.13 — rows of several degrees per warp cost
+        // LFR more than the L2 reuse saves, so one launch stays the default.
         const long long per = ((1ll << 31) - 2 * kBlock) / 32;
         for (long long r0 = 0; r0 < rows; r0 += per) {
             const int rr = static_cast<int>(std::min<long long>(per, rows - r0));

@@ -1,8 +1,8 @@
 """Device CSR construction (gqc_build_csr) against graph.cpp:25-71 semantics:
 the oracle's restatement of graphqc::Graph(n, edges, W) (pinned to the
 reference's own loader in test_ref_pin.py), the reference's own loader on a
-file through the CLI, and the facade's host build (GQC_HOST_CSR=1) byte for
-byte including the duplicate-edge warnings."""
+file through the CLI, and the facade's host build (GQC_HOST_CSR=1 vs
+GQC_DEVICE_CSR=1) byte for byte including the duplicate-edge warnings."""
 import os
 import subprocess
 
@@ -48,16 +48,16 @@ def test_device_csr_matches_oracle(n, m, weighted, seed):
     assert unit == bool(np.all(rw == 1.0))
     # conflicting duplicates: every dropped edge whose weight differs from the
     # first occurrence of its pair, ascending input index
-    first, want = {}, []
-    wa = np.ones(m) if w is None else w
-    for k in range(m):
-        if u[k] == v[k]:
-            continue
-        key = (min(u[k], v[k]), max(u[k], v[k]))
-        if key not in first:
-            first[key] = k
-        elif wa[k] != wa[first[key]]:
-            want.append((k, first[key]))
+    wa = np.ones(m) if w is None else np.asarray(w, np.float64)
+    idx = np.flatnonzero(u != v)
+    key = np.minimum(u, v).astype(np.int64)[idx] * (n + 1) + np.maximum(u, v)[idx]
+    order = np.argsort(key, kind="stable")
+    ks, ids = key[order], idx[order]
+    head = np.ones(len(ks), bool)
+    head[1:] = ks[1:] != ks[:-1]
+    first_of = ids[np.maximum.accumulate(np.where(head, np.arange(len(ks)), 0))] if len(ks) else ids
+    conf = ~head & (wa[ids] != wa[first_of])
+    want = sorted(zip(ids[conf].tolist(), first_of[conf].tolist()))
     assert dups == want[: len(dups)] and len(dups) == min(len(want), 1 << 16)
 
 
@@ -97,7 +97,8 @@ def test_cli_device_build_equals_host_build_and_reference(tmp_path):
     outs = []
     for host in ("1", "0"):
         out_csv = tmp_path / f"a{host}.csv"
-        code, out, err = run_cli(["cluster", gpath, "--sigma", "3", "--out", out_csv], {"GQC_HOST_CSR": host})
+        code, out, err = run_cli(["cluster", gpath, "--sigma", "3", "--out", out_csv],
+                                 {"GQC_HOST_CSR": host, "GQC_DEVICE_CSR": "0" if host == "1" else "1"})
         assert code == 0, err
         outs.append((out, err, open(out_csv).read()))
     assert outs[0] == outs[1]
@@ -111,7 +112,7 @@ def test_cli_device_build_equals_host_build_and_reference(tmp_path):
     lpath = tmp_path / "l.labels"
     with open(lpath, "w") as f:
         f.write("".join(f"{t} {c}\n" for t, c in lab.items()))
-    code, out, err = run_cli(["eval", lpath, lpath, "--graph", gpath], {"GQC_HOST_CSR": "0"})
+    code, out, err = run_cli(["eval", lpath, lpath, "--graph", gpath], {"GQC_DEVICE_CSR": "1"})
     assert code == 0, err
     if R.available():
         g = R.Graph.load(str(gpath))
@@ -132,7 +133,7 @@ def test_lfr_edge_file_device_build_equals_host_build(tmp_path):
     lpath = tmp_path / "lfr.labels"
     with open(lpath, "w") as f:
         f.write("\n".join(f"{i} {c}" for i, c in enumerate(lab.tolist())) + "\n")
-    code_d, out_d, err_d = run_cli(["eval", lpath, lpath, "--graph", gpath], {"GQC_HOST_CSR": "0"})
+    code_d, out_d, err_d = run_cli(["eval", lpath, lpath, "--graph", gpath], {"GQC_DEVICE_CSR": "1"})
     code_h, out_h, err_h = run_cli(["eval", lpath, lpath, "--graph", gpath], {"GQC_HOST_CSR": "1"})
     assert code_d == 0 and code_h == 0, err_d + err_h
     assert out_d == out_h

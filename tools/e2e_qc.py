@@ -35,7 +35,8 @@ def run(cmd, repeat):
         wall = time.perf_counter() - t0
         if p.returncode != 0:
             raise SystemExit(f"{cmd} failed ({p.returncode}): {p.stderr[-2000:]}")
-        trace = [l for l in p.stderr.splitlines() if l.startswith("[gqc trace]") or "sweep:" in l]
+        trace = [l for l in p.stderr.splitlines()
+                 if l.startswith("[gqc trace]") or "sweep:" in l or "load:" in l or "device init" in l]
         out.append({"wall_s": round(wall, 3), "stages_ms": stages(p.stderr), "trace": trace,
                     "stdout_tail": p.stdout[-200:]})
     return out

@@ -56,4 +56,32 @@ for gg in (u, kh):
         for q, s in enumerate([0.9, 6.0]):
             check(got[q], O.potentials_khop(gg.offsets, gg.nbr, gg.wt, 10.0, s, K))
 N.set_hop_cap(1)
+# multi-device sweep (3 shards on device 0: per-chunk output pointers, event
+# ordering, per-shard GGD) and the device CSR build
+ref, v1, _ = N.cluster_sweep(u.csr(N), sig, want_v=True)
+got, v2, _, _ = N.cluster_sweep_multi(u.csr(N), sig, [0, 0, 0], want_v=True, want_intra=True)
+check(v1, v2)
+assert all(np.array_equal(a.cluster_index, b.cluster_index) for a, b in zip(ref, got))
+rng = np.random.default_rng(1)
+eu, ev = rng.integers(0, 500, 4000).astype(np.int32), rng.integers(0, 500, 4000).astype(np.int32)
+off, nbr, wt, unit, dups = N.build_csr(500, eu, ev, rng.choice([1.0, 2.0], 4000))
+ro, rn, rw = O.csr_from_edges(500, eu, ev, None, 10.0)
+assert np.array_equal(off, ro) and np.array_equal(nbr, rn)
+# bounded chase + pointer jumping on a 5000-node monotone chain (dev_ggd)
+pth = H.path(5000)
+dp = N.DeviceCsr(pth.csr(N))
+ar = torch.arange(5000, dtype=torch.float64, device="cuda")
+Vp = torch.stack([5000.0 - ar, ar], dim=1).contiguous()
+sp = torch.empty((2, 5000), dtype=torch.int32, device="cuda"); cp = torch.empty_like(sp); cip = torch.empty_like(sp)
+ncp = torch.empty(2, dtype=torch.int32, device="cuda")
+wsp = torch.empty(N.dev_ggd_workspace(5000, 2), dtype=torch.uint8, device="cuda")
+N.dev_ggd(dp, Vp, 2, sp, cp, cip, ncp, wsp); torch.cuda.synchronize()
+assert list(ncp.cpu().numpy()) == [1, 1] and int(cp[0, 0]) == 4999 and int(cp[1, 4999]) == 0
+# polled CSR upload (>= 2^20 entries, 8 sigmas): flags released by a kernel
+big = H.random_graph(110_000, 20.0, seed=9, unit=True)
+assert big.offsets[-1] >= (1 << 20)
+res_b, vb, _ = N.cluster_sweep(big.csr(N), sig[:8], want_v=True)
+rows = np.arange(0, big.n, 9973, dtype=np.int32)
+for q, s in enumerate(sig[:8]):
+    check(vb[q][rows], O.potentials_rows(big.offsets, big.nbr, big.wt, 10.0, s, rows, workers=8))
 print("sanitize smoke ok")
