@@ -40,7 +40,7 @@
 #endif
 // GQC_WALK_EVENTS2=1: the batched walk advances both accumulators in one loop
 #ifndef GQC_WALK_EVENTS2
-#define GQC_WALK_EVENTS2 1
+#define GQC_WALK_EVENTS2 0
 #endif
 
 #ifndef GQC_LANE_OUT_SMEM
@@ -53,7 +53,10 @@ namespace gqc {
 namespace {
 
 constexpr int kBlock = 256;
-constexpr int kWarpKernelMinSigma = 8;  // below this, thread-per-(row, sigma)
+#ifndef GQC_WARP_MIN_SIGMA
+#define GQC_WARP_MIN_SIGMA 8
+#endif
+constexpr int kWarpKernelMinSigma = GQC_WARP_MIN_SIGMA;  // below this, thread-per-(row, sigma)
 // 4 x 256 threads per SM (<= 64 registers): measured best on B200 (vs 3 or 5)
 constexpr int kWarpKernelBlocksPerSM = 4;
 
