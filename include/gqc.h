@@ -256,6 +256,13 @@ gqc_status gqc_dev_resolve(int32_t n, int32_t n_sigma, const int32_t* succ_nm, i
 /* Node-major [n][n_sigma] -> sigma-major [n_sigma][n] transpose (device). */
 gqc_status gqc_dev_transpose(const double* v_nm, int32_t n, int32_t n_sigma, double* v_sm, void* stream);
 
+/* Page-locked host memory for output staging (cudaHostAlloc on GQC_OPT_DEVICE):
+ * label / field downloads into it run at PCIe speed and overlap the
+ * remaining kernels (downloads into pageable memory are queued after them).
+ * NULL on failure. */
+void* gqc_host_alloc(size_t bytes);
+void gqc_host_free(void* p);
+
 /* Number of kernel launches the last gqc_* call issued (for launch accounting). */
 int64_t gqc_last_launch_count(void);
 

@@ -587,6 +587,19 @@ const char* gqc_last_error(void) { return t_err.c_str(); }
 const char* gqc_version(void) { return "gqc 0.1 sm_100a"; }
 int64_t gqc_last_launch_count(void) { return t_launches; }
 
+void* gqc_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    const gqc_status st = guarded([&] {
+        ctx();
+        cuda_check(cudaHostAlloc(&p, std::max<size_t>(bytes, 1), cudaHostAllocDefault), "cudaHostAlloc");
+    });
+    return st == GQC_OK ? p : nullptr;
+}
+
+void gqc_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
 int32_t gqc_device_ready(void) {
     const int d = g_opt.device.load();
     return d >= 0 && d < 64 ? g_ready[d].load() : 0;
@@ -799,7 +812,9 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
         }
         // (k-hop rows read their neighbours' rows too: one slab, the whole CSR)
         const int slabs = (nnz >= (1 << 20) && t_opt.hop_cap == 1) ? 4 : 1;
-        const bool polled = slabs == 4 && !weighted && n_sigma >= 8 && polled_upload_enabled();
+        // (the warp kernel waits on the slab flags: every fast-forward sweep, or >= 8 sigmas)
+        const bool polled = slabs == 4 && !weighted && (n_sigma >= 8 || t_opt.kernel == GQC_KERNEL_FASTFWD) &&
+                            polled_upload_enabled();
         std::vector<int> bound(slabs + 1, n);
         bound[0] = 0;
         // equal-nnz row slabs; polled: growing (cumulative 10%, 30%, 60%): the

@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
+#include <thread>
 
 #include "device.hpp"
 
@@ -56,6 +58,33 @@ int max_gpus() {
 
 namespace detail {
 
+namespace {
+// Pinned host staging for label downloads (gqc_host_alloc), kept by the
+// process and grown on demand; one user at a time.
+struct PinnedStage {
+    static std::mutex& mu() {
+        static std::mutex m;
+        return m;
+    }
+    static std::pair<void*, std::size_t>& buf() {
+        static std::pair<void*, std::size_t> b{nullptr, 0};
+        return b;
+    }
+    std::unique_lock<std::mutex> lock{mu()};
+    std::int32_t* get(std::size_t count) {
+        auto& [p, cap] = buf();
+        const std::size_t bytes = std::max<std::size_t>(count, 1) * sizeof(std::int32_t);
+        if (bytes > cap) {
+            if (p) gqc_host_free(p);
+            p = gqc_host_alloc(bytes);
+            if (!p) throw std::bad_alloc();
+            cap = bytes;
+        }
+        return static_cast<std::int32_t*>(p);
+    }
+};
+}  // namespace
+
 std::vector<std::int32_t> devices_for(const Graph& g, int workers) {
     // below ~2^22 CSR entries per extra device the per-device upload and
     // context costs more than the rows it takes off the first device
@@ -78,32 +107,42 @@ std::vector<ClusterAssignment> cluster_batch_intra(const Graph& g, std::span<con
     const gqc_csr c = to_gqc(g);
     const std::vector<std::int32_t> dev = devices_for(g, workers);
     std::vector<ClusterAssignment> out(sigmas.size());
-    // bounded host staging: 64 sigmas per device call
+    // bounded host staging: 64 sigmas per device call, in pinned memory so
+    // the label downloads run at PCIe speed under the next GGD chunk; every
+    // assignment then copies its slice (in parallel over sigmas)
     constexpr std::size_t kChunk = 64;
-    std::vector<std::int32_t> center, ci, k;
+    std::vector<std::int32_t> k;
     std::vector<std::int64_t> intra;
     const bool unit = c.w == nullptr && intra_out;  // modularity's intra term comes back exact with the labels
     if (intra_out) intra_out->assign(unit ? sigmas.size() : 0, 0.0);
+    PinnedStage stage;
     for (std::size_t q0 = 0; q0 < sigmas.size(); q0 += kChunk) {
         const std::size_t m = std::min(kChunk, sigmas.size() - q0);
-        center.resize(with_center ? m * n : 0);
-        ci.resize(m * n);
+        std::int32_t* ci = stage.get(m * n * (with_center ? 2 : 1));
+        std::int32_t* center = with_center ? ci + m * n : nullptr;
         k.resize(m);
         intra.resize(unit ? m : 0);
         check(gqc_cluster_sweep_multi(&c, sigmas.data() + q0, static_cast<std::int32_t>(m), dev.data(),
-                                      static_cast<std::int32_t>(dev.size()), nullptr, nullptr,
-                                      with_center ? center.data() : nullptr, ci.data(), k.data(),
+                                      static_cast<std::int32_t>(dev.size()), nullptr, nullptr, center, ci, k.data(),
                                       unit ? intra.data() : nullptr));
-        for (std::size_t q = 0; q < m; ++q) {
-            ClusterAssignment& a = out[q0 + q];
-            a.cluster_index.assign(ci.begin() + q * n, ci.begin() + (q + 1) * n);
-            a.num_clusters = k[q];
-            if (unit) (*intra_out)[q0 + q] = static_cast<double>(intra[q]);
-            if (with_center) {
-                a.center.assign(center.begin() + q * n, center.begin() + (q + 1) * n);
-                a.centers = centers_of(a.center);
+        const unsigned T = std::max(1u, std::min<unsigned>(static_cast<unsigned>(m),
+                                                          n < 50000 ? 1u : std::thread::hardware_concurrency()));
+        auto fill = [&](std::size_t qa, std::size_t qb) {
+            for (std::size_t q = qa; q < qb; ++q) {
+                ClusterAssignment& a = out[q0 + q];
+                a.cluster_index.assign(ci + q * n, ci + (q + 1) * n);
+                a.num_clusters = k[q];
+                if (unit) (*intra_out)[q0 + q] = static_cast<double>(intra[q]);
+                if (with_center) {
+                    a.center.assign(center + q * n, center + (q + 1) * n);
+                    a.centers = centers_of(a.center);
+                }
             }
-        }
+        };
+        std::vector<std::thread> pool;
+        for (unsigned t = 1; t < T; ++t) pool.emplace_back(fill, m * t / T, m * (t + 1) / T);
+        fill(0, m / T);
+        for (std::thread& th : pool) th.join();
     }
     return out;
 }
