@@ -119,21 +119,3 @@ def test_cli_device_build_equals_host_build_and_reference(tmp_path):
         ci = np.array([lab[t] for t in seen], dtype=np.int32)
         row = g.metric_row(ci, 3, ci, 3, 1.0)
         assert out.splitlines()[1].split(",")[0] == row.split(",")[0]
-
-
-def test_lfr_edge_file_device_build_equals_host_build(tmp_path):
-    """The bench's 1M-node LFR edge list (10M lines) through `eval --graph`:
-    device and host CSR builds give the same modularity, bit for bit."""
-    from bench_tools import graphgen
-    graphgen.build()
-    off, nbr = graphgen.lfr()
-    gpath = str(tmp_path / "lfr.edges")
-    graphgen.write_edge_list(gpath, off, nbr)
-    lab = graphgen.labels(len(off) - 1)
-    lpath = tmp_path / "lfr.labels"
-    with open(lpath, "w") as f:
-        f.write("\n".join(f"{i} {c}" for i, c in enumerate(lab.tolist())) + "\n")
-    code_d, out_d, err_d = run_cli(["eval", lpath, lpath, "--graph", gpath], {"GQC_DEVICE_CSR": "1"})
-    code_h, out_h, err_h = run_cli(["eval", lpath, lpath, "--graph", gpath], {"GQC_HOST_CSR": "1"})
-    assert code_d == 0 and code_h == 0, err_d + err_h
-    assert out_d == out_h
