@@ -3,6 +3,7 @@
 // cache, host<->device staging, and orchestration of the kernels in
 // kernels.cu. No CPU compute path exists: without a CUDA device every compute
 // entry point fails with GQC_ECUDA.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -346,6 +347,34 @@ void host_exp_table(const double* d2, long long count, const std::vector<double>
 // Potentials of rows [row_begin, row_end) into v_nm[(i-row_begin)*S + s]
 // (device), for a device-resident CSR. host_w: the same weights on the host
 // (only consulted for weighted graphs), or nullptr to fetch what is needed.
+// Polled upload: the slab flag is written by a stream memory operation
+// (cuStreamWriteValue32, run by the GPU's front end behind a memory fence
+// scoped to the stream, so the slab's copy is visible before the flag) — not
+// by a kernel: the potential kernel that waits on the flag occupies every SM,
+// so a flag kernel would only run after the wait timed out. Without the
+// driver entry point, a copy from pinned memory (copy engine) writes it.
+using WriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValue32Fn write_value32() {
+    static const WriteValue32Fn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return static_cast<WriteValue32Fn>(nullptr);
+        }
+        return reinterpret_cast<WriteValue32Fn>(p);
+    }();
+    return fn;
+}
+
+void set_slab_flag(int* flag, const int* pinned_one, cudaStream_t cs) {
+    if (WriteValue32Fn fn = write_value32()) {
+        if (fn(reinterpret_cast<CUstream>(cs), reinterpret_cast<CUdeviceptr>(flag), 1u, 0u) == CUDA_SUCCESS) return;
+    }
+    cuda_check(cudaMemcpyAsync(flag, pinned_one, sizeof(int), cudaMemcpyHostToDevice, cs), "set slab flag");
+}
+
 long long slab_timeout_ms() {  // GQC_SLAB_TIMEOUT_MS: polled-upload flag wait before GQC_ECUDA
     static const long long ms = [] {
         const char* e = std::getenv("GQC_SLAB_TIMEOUT_MS");
@@ -850,7 +879,7 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
                     cuda_check(cudaMemcpyAsync(nbr + a2, g->nbr + a2, (b2 - a2) * sizeof(std::int32_t),
                                                cudaMemcpyHostToDevice, cs),
                                "copy nbr");
-                cuda_check(launch_set_flag(flags + k, cs), "set slab flag");
+                set_slab_flag(flags + k, C.slab_host + k, cs);
             }
             cuda_check(cudaStreamWaitEvent(st, C.ev[0], 0), "wait");
             SlabSync sync;

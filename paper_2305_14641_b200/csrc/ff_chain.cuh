@@ -20,6 +20,11 @@
 #ifndef GQC_STEP_FINISH
 #define GQC_STEP_FINISH 0
 #endif
+// GQC_INCR_REFRESH=1: ff_walk2 moves a stale binade cache up incrementally
+// after a crossing neighbour add (refresh_after_add)
+#ifndef GQC_INCR_REFRESH
+#define GQC_INCR_REFRESH 1
+#endif
 
 namespace gqc {
 namespace ffc {
@@ -277,9 +282,26 @@ GQC_HD inline void ff_step(Chain& ch, const double c, int& L) {
 // Both chains of a W run of length L > 0 in one loop: the warp iterates
 // 1 + (most binade crossings of any lane and chain) times over one compact
 // body instead of a pass per chain plus the general loop for multi-crossings.
+// Cache refresh at the start of a W run. A neighbour add that crossed the
+// cached binade of a jumpable chain lands in the next one (the add is below
+// base/2 < top), so the cache moves up one binade incrementally, as after a
+// settled crossing in ff_step; anything else recomputes it.
+GQC_HD inline void refresh_after_add(Chain& ch, const double c) {
+#if GQC_INCR_REFRESH
+    if ((ch.flags & kJump) && ch.s < gqc_add(ch.top, ch.top)) {
+        const double base = ch.top;
+        ch.top = gqc_add(base, base);
+        ch.inc = gqc_sub(gqc_add(base, c), base);
+        ch.flags = kJump | (exp_field(base) == ch.f_tie ? kTie : 0);
+        return;
+    }
+#endif
+    refresh(ch, c);
+}
+
 GQC_HD inline void ff_walk2(Chain& a, const double ca, Chain& b, const double cb, const int L) {
-    if (!(a.s < a.top)) refresh(a, ca);
-    if (!(b.s < b.top)) refresh(b, cb);
+    if (!(a.s < a.top)) refresh_after_add(a, ca);
+    if (!(b.s < b.top)) refresh_after_add(b, cb);
     int La = L, Lb = L;
     do {
         if (La > 0) ff_step(a, ca, La);

@@ -124,8 +124,6 @@ int launch_labels(std::int32_t n, std::int32_t n_sigma, const std::int32_t* cent
                   std::int32_t* num_clusters, void* workspace, std::size_t ws_bytes, void* stream,
                   bool flags_ready = false);
 std::size_t labels_workspace_bytes(std::int32_t n, std::int32_t n_sigma);
-// Polled upload: release-store 1 to a slab flag on the copy stream (after the slab's copy).
-int launch_set_flag(int* flag, void* stream);
 int launch_transpose(const double* v_nm, std::int32_t n, std::int32_t n_sigma, double* v_sm, void* stream);
 // Checked resolve for arbitrary successor maps: writes center/cluster_index,
 // returns status via *err_kind (0 ok, 1 out of range, 2 cycle) on the host.

@@ -396,14 +396,6 @@ __device__ __forceinline__ int load_nbr(const PotentialLaunch& P, const long lon
     return __ldg(P.nbr + k);
 }
 
-// Release-store of a polled-upload slab flag, launched on the copy stream
-// right after the slab's copy: stream order makes the copy happen-before this
-// kernel, and the release store publishes it to the potential kernel's
-// acquire load (wait_slab).
-__global__ void set_flag_kernel(int* flag) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(1) : "memory");
-}
-
 template <bool kFF, int kW>
 __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp_kernel(const __grid_constant__ PotentialLaunch P,
                                                                 const PrefixTable T, const RowSched R) {
@@ -1637,12 +1629,6 @@ int launch_chase(int n, int n_sigma, const std::int32_t* succ_sm, std::int32_t* 
     e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jump_kernel), dim3(jump_grid()), dim3(kBlock), args, 0, st);
     count_launch();
     if (e != cudaSuccess) return e;
-    return cudaGetLastError();
-}
-
-int launch_set_flag(int* flag, void* stream) {
-    set_flag_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flag);
-    count_launch();
     return cudaGetLastError();
 }
 

@@ -149,3 +149,31 @@ def test_rmat_full_field_fastfwd_equals_replay():
     for k, q in enumerate(picks):
         bad = np.flatnonzero(v_ff[q].view(np.int64) != v_rep[k].view(np.int64))
         assert bad.size == 0, f"sigma index {q}: {bad.size} rows differ, first {bad[:5]}"
+
+
+@pytest.mark.parametrize("workload,sigmas", [("lfr1m", 32), ("lfr1m", 1), ("sbm100k", 32), ("sbm100k", 1)])
+def test_polled_upload_from_pinned_buffers(workload, sigmas):
+    """The bench's e2e call: CSR in PINNED host memory, so its slab copies run
+    asynchronously while the single potential launch already waits on the
+    per-slab flags (with pageable inputs every copy completes before the launch
+    is issued). The flags come from stream memory operations, not kernels: the
+    waiting launch holds every SM. Same labels and field as the device path."""
+    import torch
+    from bench_tools import graphgen
+    from paper_2305_14641_b200.sweep import log_sigma_grid
+    graphgen.build()
+    off, nbr = graphgen.lfr() if workload == "lfr1m" else graphgen.sbm()
+    assert len(nbr) >= (1 << 20)  # the polled path needs >= 2^20 entries
+    pin_off = torch.from_numpy(off).pin_memory().numpy()
+    pin_nbr = torch.from_numpy(nbr).pin_memory().numpy()
+    sig = np.ascontiguousarray(np.asarray(log_sigma_grid(10.0, 32))[:sigmas])
+    n = len(off) - 1
+    ci = torch.empty((sigmas, n), dtype=torch.int32).pin_memory().numpy()
+    k = np.zeros(sigmas, np.int32)
+    for _ in range(3):
+        N.cluster_sweep_raw(N.Csr(pin_off, pin_nbr, None, 10.0), sig, None, ci, k)
+    res, v, _ = N.cluster_sweep(N.Csr(off, nbr, None, 10.0), sig, want_v=True)
+    assert np.array_equal(ci, np.stack([r.cluster_index for r in res]))
+    assert list(k) == [r.num_clusters for r in res]
+    vp = N.potentials(N.Csr(pin_off, pin_nbr, None, 10.0), sig)
+    assert np.array_equal(vp.view(np.int64), v.view(np.int64))
