@@ -23,7 +23,7 @@
 // GQC_INCR_REFRESH=1: ff_walk2 moves a stale binade cache up incrementally
 // after a crossing neighbour add (refresh_after_add)
 #ifndef GQC_INCR_REFRESH
-#define GQC_INCR_REFRESH 1
+#define GQC_INCR_REFRESH 0
 #endif
 
 namespace gqc {
