@@ -935,11 +935,15 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
         // with GQC_GGD_CHUNK=0 growing ones (S = 32: 4, 8, 8, 12) so the
         // downloads start after a small first chunk. Measured on LFR 1M x 32:
         // e2e 8.54 ms (16) vs 8.84 ms (growing); R-MAT 25.7 vs 27.4 ms.
+        // GQC_GGD_CHUNK=-1: shrinking chunks (S = 32: 16, 8, 4, 4), so the one
+        // download left exposed after the last GGD launch is small.
         std::vector<int> cuts{0};
         if (kGgdChunk > 0) {
             for (int s0 = kGgdChunk; s0 < n_sigma; s0 += kGgdChunk) cuts.push_back(s0);
-        } else if (n_sigma >= 16) {
+        } else if (kGgdChunk == 0 && n_sigma >= 16) {
             for (int f : {1, 3, 5}) cuts.push_back((n_sigma * f + 7) / 8);
+        } else if (kGgdChunk < 0 && n_sigma >= 16) {
+            for (int f : {4, 6, 7}) cuts.push_back((n_sigma * f + 7) / 8);
         }
         cuts.push_back(n_sigma);
         // labels of a chunk go down while the next chunk computes; into
