@@ -673,16 +673,22 @@ constexpr int kSuccUnroll = GQC_SUCC_UNROLL;    // gathers in flight per thread 
 #define GQC_SUCC_SUB 32
 #endif
 constexpr int kSuccSub = GQC_SUCC_SUB;  // sigmas per light-row argmin launch (L2-resident V slice)
+#ifndef GQC_TINY_DEGREE
+#define GQC_TINY_DEGREE 8
+#endif
+constexpr int kTinyDegree = GQC_TINY_DEGREE;  // light rows up to this degree: 16-sigma launches
 constexpr int kHeavyUnroll = GQC_HEAVY_UNROLL;  // gathers in flight per warp (heavy rows)
 
 __device__ __forceinline__ bool lex_less(double va, int ia, double vb, int ib) {
     return va < vb || (va == vb && ia < ib);
 }
 
+// Rows of degree in [deg_lo, deg_hi] only (heavy rows: successors_heavy_kernel).
 __global__ void __launch_bounds__(kBlock) successors_kernel(const long long* __restrict__ off,
                                                             const int* __restrict__ nbr,
                                                             const double* __restrict__ v, int ld, int s0, int Sc,
-                                                            int row_begin, int rows, SuccOut O) {
+                                                            int row_begin, int rows, SuccOut O, int deg_lo,
+                                                            int deg_hi) {
     // rows * Sc < 2^31 (launch_successors checks): 32-bit index math
     const unsigned tid = blockIdx.x * static_cast<unsigned>(kBlock) + threadIdx.x;
     const unsigned r = tid / static_cast<unsigned>(Sc);
@@ -690,12 +696,10 @@ __global__ void __launch_bounds__(kBlock) successors_kernel(const long long* __r
     if (r >= static_cast<unsigned>(rows)) return;
     const int s = s0 + q;
     const int i = row_begin + static_cast<int>(r);
-    // the row's own potential is loaded alongside its offsets (independent
-    // loads in flight together; an isolated row keeps best = i)
-    double vb = __ldg(v + static_cast<long long>(i) * ld + s);
     long long k = off[i];
     const long long kend = off[i + 1];
-    if (kend - k > kHeavyDegree) return;  // heavy rows: successors_heavy_kernel
+    if (kend - k > deg_hi || kend - k < deg_lo) return;
+    double vb = __ldg(v + static_cast<long long>(i) * ld + s);  // an isolated row keeps best = i
     int best = i;
     // kSuccUnroll independent gathers in flight, compared in ascending k
     for (; k + kSuccUnroll <= kend; k += kSuccUnroll) {
@@ -721,6 +725,47 @@ __global__ void __launch_bounds__(kBlock) successors_kernel(const long long* __r
         }
     }
     O.out[static_cast<long long>(r) * O.out_row + q * O.out_col] = best;
+}
+
+// Tiny rows (at most kTinyDegree neighbours, listed by mark_heavy_kernel):
+// a half-warp per row, each thread two sigmas (q and q + 16), so a warp
+// keeps two rows' gathers in flight where one tiny row per warp would leave
+// the memory system idle (R-MAT's 1-4-neighbour rows). Grid-stride over the
+// list; same lexicographic (v, id) argmin (ggd.cpp:17-19).
+__global__ void __launch_bounds__(kBlock) successors_tiny_kernel(const long long* __restrict__ off,
+                                                                 const int* __restrict__ nbr,
+                                                                 const double* __restrict__ v, int ld, int s0, int Sc,
+                                                                 int row_begin, const int* __restrict__ tiny,
+                                                                 const int* __restrict__ counts, SuccOut O) {
+    const int n_t = counts[3];
+    const int h = threadIdx.x & 15;
+    const long long step = (static_cast<long long>(gridDim.x) * blockDim.x) >> 4;
+    for (long long t = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 4; t < n_t; t += step) {
+        const int i = __ldg(tiny + t);
+        const long long kb = off[i], ke = off[i + 1];
+        const int qa = h, qb = h + 16;
+        const bool hb = qb < Sc;
+        if (qa >= Sc) continue;
+        const double* vi = v + static_cast<long long>(i) * ld + s0;
+        double va = __ldg(vi + qa), vb = hb ? __ldg(vi + qb) : 0.0;
+        int ba = i, bb = i;
+        for (long long k = kb; k < ke; ++k) {
+            const int j = __ldg(nbr + k);
+            const double* vj = v + static_cast<long long>(j) * ld + s0;
+            const double xa = __ldg(vj + qa);
+            const double xb = hb ? __ldg(vj + qb) : 0.0;
+            if (lex_less(xa, j, va, ba)) {
+                va = xa;
+                ba = j;
+            }
+            if (hb && lex_less(xb, j, vb, bb)) {
+                vb = xb;
+                bb = j;
+            }
+        }
+        O.out[static_cast<long long>(i - row_begin) * O.out_row + qa * O.out_col] = ba;
+        if (hb) O.out[static_cast<long long>(i - row_begin) * O.out_row + qb * O.out_col] = bb;
+    }
 }
 
 // Degree-class fast path of K3 (ClassOrder verified by launch_class_order):
@@ -816,13 +861,23 @@ struct HeavyRow {
     int row, slot0, nseg;
 };
 
+// Also lists the tiny rows (at most kTinyDegree neighbours, counts[3]) for
+// successors_tiny_kernel; list order does not matter (rows are independent).
 __global__ void mark_heavy_kernel(const long long* __restrict__ off, int row_begin, int rows,
-                                  HeavyItem* __restrict__ items, int* __restrict__ counts, HeavyRow* __restrict__ multi) {
+                                  HeavyItem* __restrict__ items, int* __restrict__ counts, HeavyRow* __restrict__ multi,
+                                  int* __restrict__ tiny) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= rows) return;
     const int i = row_begin + r;
-    const long long deg = off[i + 1] - off[i];
-    if (deg <= kHeavyDegree) return;
+    const long long deg = r < rows ? off[i + 1] - off[i] : kHeavyDegree + 1;
+    if (tiny) {  // warp-aggregated append
+        const bool t = r < rows && deg <= kTinyDegree;
+        const unsigned m = __ballot_sync(0xffffffffu, t);
+        int base = 0;
+        if ((threadIdx.x & 31) == 0 && m) base = atomicAdd(&counts[3], __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (t) tiny[base + __popc(m & ((1u << (threadIdx.x & 31)) - 1))] = i;
+    }
+    if (r >= rows || deg <= kHeavyDegree) return;
     const int nseg = static_cast<int>((deg + kHeavySegment - 1) / kHeavySegment);
     const int base = atomicAdd(&counts[0], nseg);
     int slot0 = -1;
@@ -1501,8 +1556,10 @@ int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nb
     const std::size_t bytes_items = sizeof(HeavyItem) * seg_max, bytes_multi = sizeof(HeavyRow) * multi_max;
     const std::size_t bytes_pv = sizeof(double) * 32 * slot_max, bytes_pi = sizeof(int) * 32 * slot_max;
     const std::size_t head = 256;
+    const bool tiny_rows = kTinyDegree > 0 && !(co && co->dir);
+    const std::size_t bytes_tiny = tiny_rows ? sizeof(int) * static_cast<std::size_t>(rows) : 0;
     void* scratch = nullptr;
-    cudaError_t e = cudaMallocFromPoolAsync(&scratch, head + bytes_pv + bytes_items + bytes_multi + bytes_pi,
+    cudaError_t e = cudaMallocFromPoolAsync(&scratch, head + bytes_pv + bytes_items + bytes_multi + bytes_pi + bytes_tiny,
                                             static_cast<cudaMemPool_t>(pool), st);
     if (e != cudaSuccess) return e;
     char* p = static_cast<char*>(scratch);
@@ -1511,8 +1568,9 @@ int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nb
     auto* items = reinterpret_cast<HeavyItem*>(p + head + bytes_pv);
     auto* multi = reinterpret_cast<HeavyRow*>(p + head + bytes_pv + bytes_items);
     int* part_i = reinterpret_cast<int*>(p + head + bytes_pv + bytes_items + bytes_multi);
+    int* tiny = tiny_rows ? reinterpret_cast<int*>(p + head + bytes_pv + bytes_items + bytes_multi + bytes_pi) : nullptr;
     cudaMemsetAsync(counts, 0, 4 * sizeof(int), st);
-    mark_heavy_kernel<<<grid_for(rows), kBlock, 0, st>>>(off, row_begin, rows, items, counts, multi);
+    mark_heavy_kernel<<<grid_for(rows), kBlock, 0, st>>>(off, row_begin, rows, items, counts, multi, tiny);
     count_launch(2);
     const int num_sms = sm_count();
     // thread = (row, sigma), sigma fastest: a neighbour's potentials for the
@@ -1538,15 +1596,21 @@ int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nb
                 successors_class_kernel<<<grid_for(static_cast<long long>(rr) * 32), kBlock, 0, st>>>(
                     off, nbr, v, ld, s0 + c0, Sc, rb, rr, Or, *co);
                 count_launch();
-            } else {
+            } else {  // rows of more than kTinyDegree neighbours (tiny ones: successors_tiny_kernel)
+                const int lo = tiny_rows ? kTinyDegree + 1 : 0;
                 for (int q0 = 0; q0 < Sc; q0 += kSuccSub) {
                     const int Sq = std::min(kSuccSub, Sc - q0);
                     const SuccOut Or{O.out + r0 * out_row + q0 * out_col, out_row, out_col};
                     successors_kernel<<<grid_for(static_cast<long long>(rr) * Sq), kBlock, 0, st>>>(
-                        off, nbr, v, ld, s0 + c0 + q0, Sq, rb, rr, Or);
+                        off, nbr, v, ld, s0 + c0 + q0, Sq, rb, rr, Or, lo, kHeavyDegree);
                     count_launch();
                 }
             }
+        }
+        if (tiny_rows) {
+            successors_tiny_kernel<<<num_sms * 8, kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, tiny, counts,
+                                                                    O);
+            count_launch();
         }
         successors_heavy_kernel<<<num_sms * 8, kBlock, 0, st>>>(off, nbr, v, ld, s0 + c0, Sc, row_begin, items, counts,
                                                                  part_v, part_i, O);
