@@ -674,7 +674,7 @@ constexpr int kSuccUnroll = GQC_SUCC_UNROLL;    // gathers in flight per thread 
 #endif
 constexpr int kSuccSub = GQC_SUCC_SUB;  // sigmas per light-row argmin launch (L2-resident V slice)
 #ifndef GQC_TINY_DEGREE
-#define GQC_TINY_DEGREE 8
+#define GQC_TINY_DEGREE 0
 #endif
 constexpr int kTinyDegree = GQC_TINY_DEGREE;  // light rows up to this degree: 16-sigma launches
 constexpr int kHeavyUnroll = GQC_HEAVY_UNROLL;  // gathers in flight per warp (heavy rows)
