@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--labels", choices=["sharded", "replicated"], default="sharded",
                     help="N > 1: labels stay with the rank owning their sigma chunk (counts all-gathered), "
                          "or are all-gathered to every rank")
+    ap.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
+                    help="N > 1: V exchange fused into the potential kernel (stores into the owner rank's buffer "
+                         "over CUDA IPC / NVLink) or an NCCL all-to-all after it")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
@@ -310,9 +313,35 @@ def run_native(args):
         N.dev_ggd(dg, v_chunk, chunk, None, center, ci_out, nc_out, ws, stream)
         launches[0] += N.last_launch_count()
 
-    with torch.cuda.stream(stream):
-        sweep = sharded.SigmaShardedSweep(n, S, rank, world, dev, pot_packed, ggd, bounds=bounds)
-    shard = sweep.send  # this rank's rows, packed by sigma chunk
+    def pot_peer(b, e, ptrs, ch):
+        N.dev_potentials_peer(dg, sig, b, e, ptrs, ch, stream)
+        launches[0] += N.last_launch_count()
+
+    # N > 1: the exchange fused into the potential kernel (PeerSigmaShardedSweep:
+    # every rank's kernel stores each sigma chunk into its owner's buffer, mapped
+    # over CUDA IPC); all ranks fall back to the NCCL all-to-all together if
+    # any rank cannot map its peers
+    sweep, exchange = None, ("none (1 GPU)" if world == 1 else "nccl all-to-all")
+    if world > 1 and args.exchange == "peer":
+        ok, err = 1, ""
+        try:
+            with torch.cuda.stream(stream):
+                sweep = sharded.PeerSigmaShardedSweep(n, S, rank, world, dev, pot_peer, ggd, bounds=bounds)
+        except Exception as ex:  # noqa: BLE001
+            ok, err = 0, str(ex)[:120]
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 1:
+            exchange = "fused: potential kernel stores into the owner rank's buffer (CUDA IPC over NVLink)"
+        else:
+            if sweep is not None:
+                sweep.close()
+            sweep = None
+            exchange = f"nccl all-to-all (peer mapping failed on a rank: {err})"
+    if sweep is None:
+        with torch.cuda.stream(stream):
+            sweep = sharded.SigmaShardedSweep(n, S, rank, world, dev, pot_packed, ggd, bounds=bounds)
+    shard = getattr(sweep, "send", None)  # world 1: this rank's rows, packed by sigma chunk
 
     def step(record=False):
         # potentials of own rows (all sigmas) -> all-to-all V by sigma chunk ->
@@ -451,7 +480,8 @@ def run_native(args):
                        "sigma_grid": f"log_sigma_grid(10, {S})", "kernel": args.kernel,
                        "distance": ("reference (graph.cpp:258-267, hop cap 1)" if args.hop_cap == 1 else
                                     f"k-hop extension, hop cap {args.hop_cap} (not a reference feature)"),
-                       "parallelism": f"potentials row-shard x{world} (cost-balanced blocks); all-to-all(V) by sigma chunk; "
+                       "exchange": exchange,
+                       "parallelism": f"potentials row-shard x{world} (cost-balanced blocks); V by sigma chunk to its owner; "
                                       f"GGD sigma-shard x{world}; "
                                       + ("all-gather(labels, counts)" if args.labels == "replicated"
                                          else "all-gather(counts), labels sharded by sigma"),

@@ -231,6 +231,29 @@ gqc_status gqc_dev_potentials_packed(const gqc_csr* g, const double* sigmas, int
                                      int32_t row_end, double* v_out, int32_t chunk, int64_t chunk_stride,
                                      void* stream);
 
+/* gqc_dev_potentials with sigma chunk q (chunk sigmas each, n_chunks =
+ * ceil(n_sigma / chunk) <= 32) of rows [row_begin, row_end) stored at
+ *     chunk_ptrs[q][(i - row_begin) * chunk + k % chunk]
+ * where each chunk_ptrs[q] is any device pointer the stream's device can
+ * store to: local, a peer device's (NVLink), or another process's buffer
+ * mapped with gqc_ipc_open. The potential kernel itself then delivers every
+ * value to the rank that owns its sigma chunk — the multi-process form of the
+ * fused exchange (no collective, no second copy of V). */
+gqc_status gqc_dev_potentials_peer(const gqc_csr* g, const double* sigmas, int32_t n_sigma, int32_t row_begin,
+                                   int32_t row_end, double* const* chunk_ptrs, int32_t n_chunks, int32_t chunk,
+                                   void* stream);
+
+/* Device memory shared between processes (CUDA IPC), on GQC_OPT_DEVICE:
+ * gqc_ipc_alloc returns a dedicated allocation and its handle
+ * (GQC_IPC_HANDLE_BYTES opaque bytes to pass to the other processes);
+ * gqc_ipc_open maps a handle from another process, gqc_ipc_close unmaps it,
+ * gqc_ipc_free releases an allocation of this process. */
+#define GQC_IPC_HANDLE_BYTES 64
+gqc_status gqc_ipc_alloc(size_t bytes, void** dev_ptr, void* handle_out);
+gqc_status gqc_ipc_open(const void* handle, void** dev_ptr);
+gqc_status gqc_ipc_close(void* dev_ptr);
+gqc_status gqc_ipc_free(void* dev_ptr);
+
 /* Scratch bytes gqc_dev_ggd needs for n nodes and n_sigma sigmas. */
 size_t gqc_dev_ggd_workspace(int32_t n, int32_t n_sigma);
 

@@ -1366,6 +1366,72 @@ gqc_status gqc_dev_potentials_packed(const gqc_csr* g, const double* sigmas, int
     });
 }
 
+gqc_status gqc_dev_potentials_peer(const gqc_csr* g, const double* sigmas, int32_t n_sigma, int32_t row_begin,
+                                   int32_t row_end, double* const* chunk_ptrs, int32_t n_chunks, int32_t chunk,
+                                   void* stream) {
+    return guarded([&] {
+        check_sigmas(sigmas, n_sigma);
+        check_csr_shape(g);
+        if (row_begin < 0 || row_end > g->n || row_begin > row_end) fail(GQC_ERANGE, "row range out of range");
+        if (chunk < 1) fail(GQC_EINVAL, "sigma chunk must be positive");
+        if (n_chunks != (n_sigma + chunk - 1) / chunk || n_chunks > kMaxShards)
+            fail(GQC_EINVAL, "chunk pointer count does not match the sigma chunks");
+        if (!chunk_ptrs) fail(GQC_EINVAL, "null output");
+        for (int q = 0; q < n_chunks; ++q)
+            if (!chunk_ptrs[q] && row_end > row_begin) fail(GQC_EINVAL, "null output");
+        DeviceCtx& C = ctx(static_cast<cudaStream_t>(stream), g->offsets);
+        double* ptr[kMaxShards] = {};
+        for (int q = 0; q < n_chunks; ++q) ptr[q] = chunk_ptrs[q];
+        if (row_end > row_begin)
+            run_potentials(C, *g, sigmas, n_sigma, row_begin, row_end, nullptr, nullptr,
+                           static_cast<cudaStream_t>(stream), nullptr, chunk, 0, nullptr, ptr);
+    });
+}
+
+gqc_status gqc_ipc_alloc(size_t bytes, void** dev_ptr, void* handle_out) {
+    return guarded([&] {
+        if (!dev_ptr || !handle_out) fail(GQC_EINVAL, "null output");
+        ctx();
+        void* p = nullptr;
+        cuda_check(cudaMalloc(&p, std::max<size_t>(bytes, 256)), "cudaMalloc");
+        cudaIpcMemHandle_t h;
+        const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            cuda_check(e, "cudaIpcGetMemHandle");
+        }
+        static_assert(sizeof(h) == GQC_IPC_HANDLE_BYTES, "IPC handle size");
+        std::memcpy(handle_out, &h, sizeof h);
+        *dev_ptr = p;
+    });
+}
+
+gqc_status gqc_ipc_open(const void* handle, void** dev_ptr) {
+    return guarded([&] {
+        if (!handle || !dev_ptr) fail(GQC_EINVAL, "null buffer");
+        ctx();
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof h);
+        void* p = nullptr;
+        cuda_check(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        *dev_ptr = p;
+    });
+}
+
+gqc_status gqc_ipc_close(void* dev_ptr) {
+    return guarded([&] {
+        ctx();
+        cuda_check(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
+    });
+}
+
+gqc_status gqc_ipc_free(void* dev_ptr) {
+    return guarded([&] {
+        ctx();
+        cuda_check(cudaFree(dev_ptr), "cudaFree");
+    });
+}
+
 size_t gqc_dev_ggd_workspace(int32_t n, int32_t n_sigma) {
     if (n < 1 || n_sigma < 1) return 0;
     return labels_workspace_bytes(n, n_sigma);

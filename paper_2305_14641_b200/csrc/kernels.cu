@@ -339,6 +339,7 @@ __global__ void __launch_bounds__(kBlock) potential_kernel(const __grid_constant
         pos = end;
     }
     *out_slot_ptr(P, i, s) = __dmul_rn(sc[0][s], __ddiv_rn(num.s, den.s));
+    if (P.out_peer) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -642,6 +643,9 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
             lane_out[static_cast<long long>(i - P.row_begin) * P.out_ld] =
                 __dmul_rn(sc[0][s], __ddiv_rn(num.s, den.s));
     }
+    // peer / IPC outputs: the stores are performed system-wide before the
+    // kernel is seen complete by the next operation in stream order
+    if (P.out_peer) __threadfence_system();
 }
 #undef pW
 #undef eW

@@ -553,6 +553,7 @@ __global__ void __launch_bounds__(kWalkBlock, kWalkBlocksPerSM)
         }
         if (lane < S) *out_slot_ptr(P, i, s) = __dmul_rn(sc[4][s], __ddiv_rn(num.s, den.s));
     }
+    if (P.out_peer) __threadfence_system();
 }
 
 int num_sms() { return sm_count(); }

@@ -84,6 +84,11 @@ def _load():
         "gqc_potentials_multi": [P, P, i32, P, i32, P],
         "gqc_row_shards": [P, i32, P],
         "gqc_build_csr": [i32, i64, P, P, P, P, P, P, P, i64, P],
+        "gqc_dev_potentials_peer": [P, P, i32, i32, i32, P, i32, i32, P],
+        "gqc_ipc_alloc": [C.c_size_t, P, P],
+        "gqc_ipc_open": [P, P],
+        "gqc_ipc_close": [P],
+        "gqc_ipc_free": [P],
         "gqc_dev_potentials": [P, P, i32, i32, i32, P, P],
         "gqc_dev_potentials_packed": [P, P, i32, i32, i32, P, i32, i64, P],
         "gqc_dev_ggd": [P, P, i32, P, P, P, P, P, C.c_size_t, P],
@@ -430,6 +435,63 @@ def dev_potentials_packed(dg: DeviceCsr, sigmas, row_begin: int, row_end: int, o
     sp = None if stream is None else C.c_void_p(stream.cuda_stream)
     _check(_lib.gqc_dev_potentials_packed(C.byref(cs), _ptr(s), len(s), int(row_begin), int(row_end),
                                           C.c_void_p(out.data_ptr()), int(chunk), int(chunk_stride), sp))
+
+
+def dev_potentials_peer(dg: DeviceCsr, sigmas, row_begin: int, row_end: int, chunk_ptrs, chunk: int, stream=None):
+    """gqc_dev_potentials_peer: sigma chunk q of rows [row_begin, row_end) to
+    chunk_ptrs[q] + ((i - row_begin) * chunk + k % chunk) * 8 (raw device
+    addresses: local, peer or IPC-mapped)."""
+    s = np.ascontiguousarray(np.atleast_1d(np.asarray(sigmas, dtype=np.float64)))
+    ptrs = (C.c_void_p * len(chunk_ptrs))(*[int(p) for p in chunk_ptrs])
+    cs = dg.c_struct()
+    sp = None if stream is None else C.c_void_p(stream.cuda_stream)
+    _check(_lib.gqc_dev_potentials_peer(C.byref(cs), _ptr(s), len(s), int(row_begin), int(row_end), ptrs,
+                                        len(chunk_ptrs), int(chunk), sp))
+
+
+IPC_HANDLE_BYTES = 64
+
+
+class IpcBuffer:
+    """Device memory another process can map (gqc_ipc_alloc), exposed to torch
+    through __cuda_array_interface__ (zero copy)."""
+
+    def __init__(self, nbytes: int):
+        p = C.c_void_p()
+        self.handle = C.create_string_buffer(IPC_HANDLE_BYTES)
+        _check(_lib.gqc_ipc_alloc(int(nbytes), C.byref(p), self.handle))
+        self.ptr = int(p.value)
+        self.nbytes = int(nbytes)
+
+    def handle_bytes(self) -> bytes:
+        return self.handle.raw
+
+    def as_tensor(self, dtype, shape, device):
+        import torch
+        itemsize = torch.empty((), dtype=dtype).element_size()
+        typestr = {torch.float64: "<f8", torch.int32: "<i4", torch.float32: "<f4"}[dtype]
+        holder = type("CudaArray", (), {})()
+        holder.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (self.ptr, False),
+                                           "version": 2, "strides": None}
+        assert int(np.prod(shape)) * itemsize <= self.nbytes
+        return torch.as_tensor(holder, device=device)
+
+    def free(self):
+        if self.ptr:
+            _check(_lib.gqc_ipc_free(C.c_void_p(self.ptr)))
+            self.ptr = 0
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map another process's gqc_ipc_alloc buffer on GQC_OPT_DEVICE; returns its address here."""
+    p = C.c_void_p()
+    buf = C.create_string_buffer(bytes(handle), IPC_HANDLE_BYTES)
+    _check(_lib.gqc_ipc_open(buf, C.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr: int):
+    _check(_lib.gqc_ipc_close(C.c_void_p(int(ptr))))
 
 
 def dev_ggd_workspace(n: int, n_sigma: int) -> int:

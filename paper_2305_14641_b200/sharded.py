@@ -203,3 +203,109 @@ class SigmaShardedSweep:
         v = self.exchange()
         self.ggd(v)
         return self.gather()
+
+
+class PeerSigmaShardedSweep:
+    """SigmaShardedSweep with the exchange fused into the potential kernel
+    (gqc_dev_potentials_peer): every rank maps every other rank's receive
+    buffer (CUDA IPC, gqc_ipc_alloc / gqc_ipc_open), and its potential kernel
+    stores sigma chunk q of its rows straight into rank q's node-major
+    V[n][chunk] over NVLink — no all-to-all and no second copy of V. One
+    stream-ordered all-reduce of one float per step (NCCL; with gloo a device
+    sync + barrier) orders every rank's stores before any rank's GGD reads its
+    chunk; receive buffers alternate between steps, so the next step's stores
+    never race the previous step's GGD (a rank passes step k+1's barrier only
+    after every rank's step-k GGD, which precedes it on that rank's stream).
+
+      potentials_peer(begin, end, chunk_ptrs, chunk): raw device addresses,
+          chunk_ptrs[q] = where row `begin` of sigma chunk q goes
+      ggd(V_chunk [n, chunk] node-major, ci [chunk, n] int32, nc [chunk] int32)
+    """
+
+    def __init__(self, n, n_sigma, rank, world, device, potentials_peer, ggd, group=None, bounds=None):
+        from . import native as N
+        self.n, self.S, self.rank, self.world, self.group = n, n_sigma, rank, world, group
+        if bounds is None:
+            bounds = [row_shard(n, world, r)[0] for r in range(world)] + [n]
+        self.bounds = [int(b) for b in bounds]
+        self.begin, self.end = self.bounds[rank], self.bounds[rank + 1]
+        self.rows = self.end - self.begin
+        self.chunk = sigma_chunk(n_sigma, world)
+        self.n_chunks = (n_sigma + self.chunk - 1) // self.chunk
+        self.s_begin, self.s_end = sigma_shard(n_sigma, world, rank)
+        self.potentials_peer, self.ggd_op = potentials_peer, ggd
+        nbytes = max(1, n * self.chunk) * 8
+        self.bufs = [N.IpcBuffer(nbytes) for _ in range(2)]
+        mine = [b.handle_bytes() for b in self.bufs]
+        if world > 1:
+            allh = [None] * world
+            dist.all_gather_object(allh, mine, group=group)
+        else:
+            allh = [mine]
+        self.mapped = []
+        self.peer = []  # peer[k][q]: base address of rank q's buffer k in this process
+        for k in range(2):
+            row = []
+            for q in range(world):
+                if q == rank:
+                    row.append(self.bufs[k].ptr)
+                else:
+                    a = N.ipc_open(allh[q][k])
+                    self.mapped.append(a)
+                    row.append(a)
+            self.peer.append(row)
+        self.views = [b.as_tensor(torch.float64, (n, self.chunk), device) for b in self.bufs]
+        self.ci = torch.zeros((self.chunk, n), dtype=torch.int32, device=device)
+        self.nc = torch.zeros(self.chunk, dtype=torch.int32, device=device)
+        self.nc_full = torch.empty(world * self.chunk, dtype=torch.int32, device=device) if world > 1 else self.nc
+        self.ci_full = torch.empty((world * self.chunk, n), dtype=torch.int32, device=device) if world > 1 else self.ci
+        self.tick = torch.zeros(1, dtype=torch.float32, device=device)
+        self.nccl = world > 1 and dist.get_backend(group) == "nccl"
+        self.step_k = 0
+
+    def potentials(self):
+        k = self.step_k & 1
+        if self.rows > 0:
+            ptrs = [self.peer[k][q] + self.begin * self.chunk * 8 for q in range(self.n_chunks)]
+            self.potentials_peer(self.begin, self.end, ptrs, self.chunk)
+
+    def exchange(self):
+        """Orders every rank's stores before this rank's GGD; returns V[n, chunk]."""
+        if self.world > 1:
+            if self.nccl:
+                dist.all_reduce(self.tick, group=self.group)
+            else:
+                torch.cuda.synchronize()
+                dist.barrier(group=self.group)
+        v = self.views[self.step_k & 1]
+        self.step_k += 1
+        return v
+
+    def ggd(self, v_chunk):
+        if self.s_end > self.s_begin:
+            self.ggd_op(v_chunk, self.ci, self.nc)
+
+    def gather_counts(self):
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.nc_full, self.nc, group=self.group)
+        return self.nc_full[: self.S]
+
+    def gather(self):
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.ci_full, self.ci, group=self.group)
+            dist.all_gather_into_tensor(self.nc_full, self.nc, group=self.group)
+        return self.ci_full[: self.S], self.nc_full[: self.S]
+
+    def step(self):
+        self.potentials()
+        self.ggd(self.exchange())
+        return self.gather()
+
+    def close(self):
+        from . import native as N
+        torch.cuda.synchronize()
+        for a in self.mapped:
+            N.ipc_close(a)
+        self.mapped = []
+        for b in self.bufs:
+            b.free()
