@@ -356,6 +356,11 @@ constexpr int kPrefixStride = kPrefixCap + 1;
 #define GQC_BATCH_MIN_DEGREE 32
 #endif
 constexpr int kBatchMinDegree = GQC_BATCH_MIN_DEGREE;  // padded: no bank conflicts across lanes
+// Rows with at least this many neighbours walk the whole row at once (0: never).
+#ifndef GQC_LONG_ROW
+#define GQC_LONG_ROW 1024
+#endif
+constexpr int kLongRow = GQC_LONG_ROW;
 
 // Polled CSR upload: lane 0 waits (acquire) until the copy stream has set
 // the flag of row i's slab; a flag that never arrives sets *slab_err after
@@ -579,7 +584,58 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
                 den.top = 0.0;
                 pos = cols[j1 - 1] + 1;
             };
-            for (long long base = kbeg; base < kend; base += 32) {
+            if (kLongRow > 0 && kend - kbeg >= kLongRow) {
+                // Long rows (R-MAT's hubs): one walk over the whole row, its
+                // binary searches reading the CSR row directly (cached), so a
+                // row costs O(crossings x log deg) instead of one staged
+                // 32-event chunk after another — a hub of 10^5 neighbours was
+                // a ~3-4 ms sequential chain for its warp, the critical path of
+                // a sharded R-MAT sweep.
+                const int deg = static_cast<int>(kend - kbeg);
+                const struct {
+                    const PotentialLaunch* P;
+                    long long b;
+                    __device__ int operator()(int q) const { return load_nbr(*P, b + q); }
+                } colg{&P, kbeg};
+                auto walkg = [&](const int j0, const int j1) {
+                    num.s = walk_events(num.s, pW, p1, tie_num, tie_p1, colg, j0, j1, pos);
+                    den.s = walk_events(den.s, eW, e1, tie_den, tie_e1, colg, j0, j1, pos);
+                    num.top = 0.0;
+                    den.top = 0.0;
+                    pos = colg(j1 - 1) + 1;
+                };
+                const int jend = (tail && colg(deg - 1) == n - 1) ? deg - 1 : deg;
+                int before_self = 0;  // neighbours below the row's own column
+                {
+                    int hi = deg;
+                    while (before_self < hi) {
+                        const int mid = (before_self + hi) >> 1;
+                        if (colg(mid) < i) before_self = mid + 1;
+                        else hi = mid;
+                    }
+                }
+                int j = 0;
+                while (j < deg) {  // warp-uniform
+                    if (pos == 0 || j >= jend) {  // first event of the row, or the tail neighbour
+                        event(colg(j), kbeg + j, 1.0);
+                        ++j;
+                        continue;
+                    }
+                    int r = jend;
+                    if (self_pending) r = min(max(before_self, j), jend);
+                    if (r > j) {
+                        walkg(j, r);
+                        j = r;
+                    }
+                    if (self_pending && j < jend) {
+                        w_run(num, den, pos, i - pos);
+                        den.s = __dadd_rn(den.s, 1.0);
+                        pos = i + 1;
+                        self_pending = false;
+                    }
+                }
+            }
+            for (long long base = kbeg; base < kend && !(kLongRow > 0 && kend - kbeg >= kLongRow); base += 32) {
                 const int cnt = static_cast<int>(min(32ll, kend - base));
                 const int my = lane < cnt ? load_nbr(P, base + lane) : n;
                 __syncwarp();
