@@ -402,7 +402,11 @@ __device__ __forceinline__ int load_nbr(const PotentialLaunch& P, const long lon
     return __ldg(P.nbr + k);
 }
 
-template <bool kFF, int kW>
+// kLong: rows of >= kLongRow neighbours walk the whole row at once (used for
+// row-range launches, i.e. shards of a multi-device sweep, where the longest
+// row is the critical path; a whole-graph launch keeps the chunked walk, which
+// measured faster for throughput and does not carry the extra code).
+template <bool kFF, int kW, bool kLong = false>
 __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp_kernel(const __grid_constant__ PotentialLaunch P,
                                                                 const PrefixTable T, const RowSched R) {
     __shared__ double sc[kSigmaFields][kMaxSigmaPerLaunch];
@@ -584,7 +588,7 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
                 den.top = 0.0;
                 pos = cols[j1 - 1] + 1;
             };
-            if (kLongRow > 0 && kend - kbeg >= kLongRow) {
+            if constexpr (kLong) if (kLongRow > 0 && kend - kbeg >= kLongRow) {
                 // Long rows (R-MAT's hubs): one walk over the whole row, its
                 // binary searches reading the CSR row directly (cached), so a
                 // row costs O(crossings x log deg) instead of one staged
@@ -635,7 +639,8 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
                     }
                 }
             }
-            for (long long base = kbeg; base < kend && !(kLongRow > 0 && kend - kbeg >= kLongRow); base += 32) {
+            for (long long base = kbeg; base < kend && !(kLong && kLongRow > 0 && kend - kbeg >= kLongRow);
+                 base += 32) {
                 const int cnt = static_cast<int>(min(32ll, kend - base));
                 const int my = lane < cnt ? load_nbr(P, base + lane) : n;
                 __syncwarp();
@@ -1328,7 +1333,10 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
         };
         switch (p.weight_mode) {
             case kUnit:
-                if (ff) launch(potential_warp_kernel<true, kUnit>);
+                // a row range short of the whole graph is a shard of a
+                // multi-device sweep: hub rows walk whole (kLong)
+                if (ff && p.row_end - p.row_begin < p.n) launch(potential_warp_kernel<true, kUnit, true>);
+                else if (ff) launch(potential_warp_kernel<true, kUnit>);
                 else launch(potential_warp_kernel<false, kUnit>);
                 break;
             case kDevicePexp:

@@ -88,12 +88,15 @@ def test_khop_extension_multi():
         N.set_hop_cap(1)
 
 
-@pytest.mark.parametrize("workload", ["sbm100k", "lfr1m"])
+@pytest.mark.parametrize("workload", ["sbm100k", "lfr1m", "rmat22"])
 def test_bench_graphs_eight_shards(workload):
+    """8 shards of the bench graphs; on R-MAT the shards' launches walk hub rows
+    (>= 1024 neighbours) whole (kLong) while the single-device launch uses the
+    chunked walk, so this also pins the two walks to each other bit for bit."""
     from bench_tools import graphgen
     from paper_2305_14641_b200.sweep import log_sigma_grid
     graphgen.build()
-    off, nbr = graphgen.sbm() if workload == "sbm100k" else graphgen.lfr()
+    off, nbr = {"sbm100k": graphgen.sbm, "lfr1m": graphgen.lfr, "rmat22": graphgen.rmat}[workload]()
     check_multi(N.Csr(off, nbr, None, 10.0), np.asarray(log_sigma_grid(10.0, 32)), 8, intra=True)
 
 
