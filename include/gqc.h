@@ -285,6 +285,11 @@ gqc_status gqc_dev_transpose(const double* v_nm, int32_t n, int32_t n_sigma, dou
  * NULL on failure. */
 void* gqc_host_alloc(size_t bytes);
 void gqc_host_free(void* p);
+/* Page-lock an existing host range (cudaHostRegister) / release it: a CSR
+ * the caller keeps across calls then uploads at PCIe speed, under the
+ * potential launch (the CLI registers its graph while it reads the labels). */
+gqc_status gqc_host_register(void* p, size_t bytes);
+gqc_status gqc_host_unregister(void* p);
 
 /* Number of kernel launches the last gqc_* call issued (for launch accounting). */
 int64_t gqc_last_launch_count(void);

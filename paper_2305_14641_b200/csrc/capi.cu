@@ -629,6 +629,22 @@ void gqc_host_free(void* p) {
     if (p) cudaFreeHost(p);
 }
 
+gqc_status gqc_host_register(void* p, size_t bytes) {
+    return guarded([&] {
+        if (!p || bytes == 0) return;
+        ctx();
+        cuda_check(cudaHostRegister(p, bytes, cudaHostRegisterDefault), "cudaHostRegister");
+    });
+}
+
+gqc_status gqc_host_unregister(void* p) {
+    return guarded([&] {
+        if (!p) return;
+        ctx();
+        cuda_check(cudaHostUnregister(p), "cudaHostUnregister");
+    });
+}
+
 int32_t gqc_device_ready(void) {
     const int d = g_opt.device.load();
     return d >= 0 && d < 64 ? g_ready[d].load() : 0;
