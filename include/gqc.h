@@ -106,8 +106,9 @@ gqc_status gqc_get_option(gqc_option key, int64_t* value);
 int32_t gqc_device_count(void);
 /* Optional: create the current device's context, streams and memory pool and
  * load the sweep kernels now (every entry point otherwise does this on first
- * use). Safe to call from a helper thread while the caller parses its input,
- * as long as no other gqc_* call runs concurrently. No reference counterpart
+ * use). Safe to call from a helper thread while the caller parses its input
+ * (it holds the device's lock; other calls on that device wait for it). No
+ * reference counterpart
  * (the reference has no device); the CLI uses it to overlap CUDA start-up
  * (~0.5-1.5 s per process) with edge-list parsing. */
 gqc_status gqc_init(void);

@@ -670,9 +670,8 @@ static std::vector<int> option_devices();
 gqc_status gqc_init(void) {
     return guarded([&] {
         ctx();
-        // one tiny sweep on the warp-per-row path (8 sigmas) and on the
-        // thread-per-row path (1 sigma): creates the context's streams and
-        // pool and loads the modules of the kernels a sweep launches
+        // two tiny sweeps (8 sigmas and 1): create the context's streams and
+        // pool and load the modules of the kernels a sweep launches
         const std::int64_t off[4] = {0, 1, 3, 4};
         const std::int32_t nbr[4] = {1, 0, 2, 1};
         const gqc_csr g{3, 4, off, nbr, nullptr, 10.0};
