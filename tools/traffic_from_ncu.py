@@ -37,8 +37,10 @@ FIELDS = {
 def kernel_key(name):
     m = re.search(r"(\w+)<([^>]*)>\s*\(", name)
     if m and m.group(1) == "potential_warp_kernel":
-        ff, w = [a.strip() for a in m.group(2).split(",")]
-        return f"potential_warp_kernel<{'FASTFWD' if ff == '1' else 'REPLAY'},{ {'0': 'unit', '1': 'pexp', '2': 'table'}[w] }>"
+        args = [a.strip() for a in m.group(2).split(",")]
+        ff, w = args[0], args[1]
+        key = f"potential_warp_kernel<{'FASTFWD' if ff == '1' else 'REPLAY'},{ {'0': 'unit', '1': 'pexp', '2': 'table'}[w] }"
+        return key + (",long>" if len(args) > 2 and args[2] in ("1", "true") else ">")
     m = re.search(r"(\w+)(<[^(]*>)?\s*\(", name)
     return m.group(1) if m else name
 
