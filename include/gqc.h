@@ -12,8 +12,15 @@
  *   gqc_resolve_centers     <- graphqc::resolve_centers (ggd.hpp:33, ggd.cpp:26-57)
  *   gqc_cluster_sweep       <- graphqc::cluster (ggd.hpp:37, ggd.cpp:59-62) for every sigma of a
  *                              grid, i.e. the per-sigma loop of graphqc::run_sweep (sweep.cpp:50-57)
+ *   gqc_cluster_sweep_multi,
+ *   gqc_potentials_multi    <- compute_potentials_parallel(g, sigma, workers) (potential.cpp:62-87)
+ *                              with GPUs as the workers, for cluster / run_sweep; the n_gpus
+ *                              parameter of the survey's gqc_potentials / gqc_cluster_sweep is
+ *                              GQC_OPT_GPUS (same entry points) or the explicit device list here
+ *   gqc_build_csr           <- graphqc::Graph(n, edges, W)'s CSR (graph.cpp:25-71), on the device
  *   gqc_dev_*               <- the same operations on device-resident buffers (row-sharded
- *                              potentials for multi-GPU; the collective lives in the host layer)
+ *                              potentials for multi-GPU, incl. gqc_dev_potentials_peer whose
+ *                              kernel stores each sigma chunk into its owner's buffer)
  *
  * Conventions: plain pointers and sizes, no C++ or torch types. Host-buffer
  * entry points (gqc_potentials, gqc_build_successors, gqc_resolve_centers,
