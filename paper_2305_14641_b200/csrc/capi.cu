@@ -953,7 +953,16 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
         // GQC_GGD_CHUNK=-1: shrinking chunks (S = 32: 16, 8, 4, 4), so the one
         // download left exposed after the last GGD launch is small.
         std::vector<int> cuts{0};
-        if (kGgdChunk > 0) {
+        if (const char* e = std::getenv("GQC_GGD_CUTS"); e && *e && n_sigma >= 2) {
+            // measurement knob: chunk sizes as a comma list, e.g. "4,8,8,12"
+            for (const char* p = e; *p;) {
+                char* q = nullptr;
+                const long c = std::strtol(p, &q, 10);
+                if (q == p) break;
+                if (c > 0 && cuts.back() + c < n_sigma) cuts.push_back(cuts.back() + static_cast<int>(c));
+                p = *q ? q + 1 : q;
+            }
+        } else if (kGgdChunk > 0) {
             for (int s0 = kGgdChunk; s0 < n_sigma; s0 += kGgdChunk) cuts.push_back(s0);
         } else if (kGgdChunk == 0 && n_sigma >= 16) {
             for (int f : {1, 3, 5}) cuts.push_back((n_sigma * f + 7) / 8);
