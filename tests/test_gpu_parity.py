@@ -618,9 +618,11 @@ def test_device_binding_follows_stream_and_option():
 def test_degree_class_order_fast_path_matches_plain_argmin():
     """Opt-in GGD argmin fast path (GQC_CLASS_ORDER=1, launch_class_order):
     on unit-weight graphs the degree classes order the potentials for most
-    sigmas and only the best class is gathered. Same labels as the plain
-    argmin (default, a separate process) and as the oracle; weighted fields
-    skip it."""
+    sigmas and only the best class is gathered. Same successor maps (every
+    entry) and labels as the plain argmin (default, a separate process) and
+    as the oracle, also on a graph with hub rows (heavy-row argmin next to
+    class-ordered light rows) and isolated nodes; the trace shows the verified
+    sigmas; weighted fields skip it."""
     import json
     import subprocess
     import sys
@@ -630,28 +632,56 @@ import numpy as np
 sys.path.insert(0, ".")
 from paper_2305_14641_b200 import native as N
 from tests import helpers as H
+import hashlib
 out = {}
-for name, g in [("sbm", None), ("rand", H.random_graph(3001, 14, 21, unit=True)),
+def hub_graph():
+    # 20k nodes: 3 hubs of degree ~3000 (above the class cap), 40 of ~150
+    # (global-atomic classes), a sparse random rest, 50 isolated nodes
+    rng = np.random.default_rng(5)
+    n = 20000
+    e = set()
+    for h, d in [(0, 3100), (7777, 2600), (19999, 3000)] + [(int(x), 150) for x in rng.choice(np.arange(100, 19000), 40, replace=False)]:
+        for j in rng.choice(n - 50, d, replace=False):
+            if j != h: e.add((min(h, j), max(h, j)))
+    for _ in range(60000):
+        a, b = rng.integers(0, n - 50, 2)
+        if a != b: e.add((min(a, b), max(a, b)))
+    rows = [[] for _ in range(n)]
+    for a, b in e:
+        rows[a].append(b); rows[b].append(a)
+    off = np.zeros(n + 1, np.int64); off[1:] = np.cumsum([len(r) for r in rows])
+    nbr = np.concatenate([np.sort(np.array(r, np.int32)) for r in rows if r]).astype(np.int32)
+    return N.Csr(off, nbr, None, 10.0)
+for name, g in [("sbm", None), ("rand", H.random_graph(3001, 14, 21, unit=True)), ("hubs", "hubs"),
                 ("weighted", H.random_graph(2001, 9, 22, unit=False))]:
     if g is None:
         off, nbr = H.sbm_csr()
         csr = N.Csr(off, nbr, None, 10.0)
+    elif g == "hubs":
+        csr = hub_graph()
     else:
         csr = g.csr(N)
     res, _, succ = N.cluster_sweep(csr, np.exp(np.linspace(0.0, np.log(30.0), 32)), want_succ=True)
-    out[name] = [int(np.frombuffer(succ.tobytes(), np.uint8).astype(np.int64).sum()), N.last_launch_count(),
-                 [r.num_clusters for r in res], succ.tolist()[::97]]
+    out[name] = [hashlib.sha256(succ.tobytes()).hexdigest(), N.last_launch_count(),
+                 [r.num_clusters for r in res], hashlib.sha256(b"".join(r.cluster_index.tobytes() for r in res)).hexdigest()]
 print(json.dumps(out))
 '''
     import os
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     runs = {}
+    traces = {}
     for flag in ("1", "0"):  # GQC_CLASS_ORDER: on / off
         r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
-                           env=dict(os.environ, GQC_CLASS_ORDER=flag))
+                           env=dict(os.environ, GQC_CLASS_ORDER=flag, GQC_TRACE="1"))
         assert r.returncode == 0, r.stderr[-2000:]
         runs[flag] = json.loads(r.stdout.strip().splitlines()[-1])
-    for name in ("sbm", "rand", "weighted"):
+        traces[flag] = [ln for ln in r.stderr.splitlines() if "class order:" in ln]
+    # three unit-weight sweeps ordered their classes (most sigmas verified)
+    assert len(traces["1"]) == 3 and not traces["0"], traces
+    for ln in traces["1"]:
+        dirs = [int(x) for x in ln.split("dir =")[1].split()]
+        assert len(dirs) == 32 and sum(d != 0 for d in dirs) >= 16, ln
+    for name in ("sbm", "rand", "hubs", "weighted"):
         on, off = runs["1"][name], runs["0"][name]
         assert on[0] == off[0] and on[2] == off[2] and on[3] == off[3], name
         # the class-order launches ran (unit weights) / were skipped (weighted)
