@@ -215,7 +215,7 @@ int* pinned_counts_buf(int*& buf, int& cap, int n) {
 int* pinned_counts(DeviceCtx& C, int n) { return pinned_counts_buf(C.nc_host, C.nc_host_cap, n); }
 
 // Device word the bounded chase sets when a successor map has a cycle
-// (launch_chase), cleared on `st`; its pinned readback slot.
+// (launch_labels), cleared on `st`; its pinned readback slot.
 int* ggd_err_word(DevBuf& buf, int*& host, cudaStream_t st) {
     int* d = buf.get<int>(1);
     cuda_check(cudaMemsetAsync(d, 0, sizeof(int), st), "clear error word");
@@ -997,8 +997,7 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
             cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, s0, Sc, 0, n, ds + o, 1, n, nnz, C.pool, st,
                                          order.get()),
                        "successor kernel");
-            cuda_check(launch_chase(n, Sc, ds + o, dc + o, st, ws, d_err), "chase kernel");
-            cuda_check(launch_labels(n, Sc, dc + o, dci + o, dnc + s0, ws, wsb, st, true), "label kernels");
+            cuda_check(launch_labels(n, Sc, ds + o, dc + o, dci + o, dnc + s0, ws, wsb, st, d_err), "label kernels");
             if (intra_out)
                 cuda_check(launch_intra_counts(n, Sc, d.offsets, d.nbr, dci + o, d_intra + s0, st), "intra counts");
             tr.mark("ggd_chunk");
@@ -1211,8 +1210,7 @@ static void sweep_multi_impl(const gqc_csr* g, const double* sigmas, int S, cons
                                      order.get()),
                    "successor kernel");
         int* d_err = ggd_err_word(Bq.err, Bq.err_host, st);
-        cuda_check(launch_chase(n, Sq, ds, dc, st, ws, d_err), "chase kernel");
-        cuda_check(launch_labels(n, Sq, dc, dci, dnc, ws, wsb, st, true), "label kernels");
+        cuda_check(launch_labels(n, Sq, ds, dc, dci, dnc, ws, wsb, st, d_err), "label kernels");
         cuda_check(cudaMemcpyAsync(Bq.err_host, d_err, sizeof(int), cudaMemcpyDeviceToHost, st), "copy error word");
         if (intra_out)
             cuda_check(launch_intra_counts(n, Sq, dg.offsets, dg.nbr, dci, Bq.intra.get<long long>(Sq), st),
@@ -1477,8 +1475,7 @@ gqc_status gqc_dev_ggd(const gqc_csr* g, const double* v, int32_t n_sigma, int32
         cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, 0, g->n, s, 1, g->n, g->nnz, C.pool,
                                      st, order.get()),
                    "successor kernel");
-        cuda_check(launch_chase(g->n, n_sigma, s, center, st, workspace), "chase kernel");
-        cuda_check(launch_labels(g->n, n_sigma, center, cluster_index, num_clusters, workspace, workspace_bytes, st, true),
+        cuda_check(launch_labels(g->n, n_sigma, s, center, cluster_index, num_clusters, workspace, workspace_bytes, st),
                    "label kernels");
     });
 }
@@ -1514,8 +1511,7 @@ gqc_status gqc_dev_resolve(int32_t n, int32_t n_sigma, const int32_t* succ_nm, i
         auto st = static_cast<cudaStream_t>(stream);
         bind_device(st, succ_nm);
         cuda_check(launch_transpose_i32(succ_nm, n, n_sigma, center, st), "transpose");
-        cuda_check(launch_chase(n, n_sigma, center, center, st, workspace), "chase kernel");
-        cuda_check(launch_labels(n, n_sigma, center, cluster_index, num_clusters, workspace, workspace_bytes, st, true),
+        cuda_check(launch_labels(n, n_sigma, center, center, cluster_index, num_clusters, workspace, workspace_bytes, st),
                    "label kernels");
     });
 }

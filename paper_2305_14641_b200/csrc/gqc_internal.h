@@ -114,15 +114,15 @@ int launch_successors(std::int32_t n, const std::int64_t* offsets, const std::in
 int launch_intra_counts(std::int32_t n, std::int32_t n_sigma, const std::int64_t* offsets, const std::int32_t* nbr,
                         const std::int32_t* ci_sm, long long* out, void* stream);
 int launch_transpose_i32(const std::int32_t* in, std::int32_t n, std::int32_t n_sigma, std::int32_t* out, void* stream);
-// labels_workspace: launch_labels' workspace (required); the chase writes the
-// center flags there (call launch_labels with flags_ready) and keeps its
-// status words there. err (optional, device): set to 1 if a map has a cycle
-// (bounded chase + pointer jumping, see chase_kernel).
-int launch_chase(std::int32_t n, std::int32_t n_sigma, const std::int32_t* succ_sm, std::int32_t* center_sm,
-                 void* stream, void* labels_workspace, std::int32_t* err = nullptr);
-int launch_labels(std::int32_t n, std::int32_t n_sigma, const std::int32_t* center_sm, std::int32_t* cluster_index_sm,
-                  std::int32_t* num_clusters, void* workspace, std::size_t ws_bytes, void* stream,
-                  bool flags_ready = false);
+// GGD chase + labels (K4/K5, ggd.cpp:26-57) for n_sigma sigma-major slices:
+// center = the root of every node's successor chain (succ_sm == center_sm:
+// in place), cluster_index = the root's rank among the ascending roots,
+// num_clusters (device) per sigma. workspace: labels_workspace_bytes(n,
+// n_sigma) bytes (required). err (optional, device): set to 1 if a map has a
+// cycle (bounded chase + pointer jumping, see chase_kernel).
+int launch_labels(std::int32_t n, std::int32_t n_sigma, const std::int32_t* succ_sm, std::int32_t* center_sm,
+                  std::int32_t* cluster_index_sm, std::int32_t* num_clusters, void* workspace, std::size_t ws_bytes,
+                  void* stream, std::int32_t* err = nullptr);
 std::size_t labels_workspace_bytes(std::int32_t n, std::int32_t n_sigma);
 int launch_transpose(const double* v_nm, std::int32_t n, std::int32_t n_sigma, double* v_sm, void* stream);
 // Checked resolve for arbitrary successor maps: writes center/cluster_index,

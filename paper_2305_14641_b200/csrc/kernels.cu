@@ -1064,30 +1064,121 @@ __global__ void transpose_i32_kernel(const int* __restrict__ in, int n, int S, i
     }
 }
 
-// K4: chase successors to their fixed point. center[] starts as a copy of
-// succ; every thread follows pointers through center[], which other threads
-// overwrite with roots as they finish (any value read is an ancestor, so the
-// result is exact; finished neighbours shorten the walk). Maps built by K3
-// strictly decrease (v, id) along a chain, so every walk terminates — but a
-// long monotone chain would cost one thread O(depth) dependent loads, so a
-// walk stops after kChaseSteps, leaves the ancestor it reached and counts
-// itself pending; jump_kernel then finishes by pointer jumping in at most
-// ceil(log2 n) + 2 synchronous rounds (or reports a cycle, ggd.cpp:41).
-// With flag != nullptr it also writes the center flags of K5a (flag[b + i] =
-// root == i, i.e. succ[i] == i: roots are known before any chasing).
+// K4/K5: successor chase and labels (ggd.cpp:26-57).
+// roots_kernel reads succ once: it copies it into center[] (unless in place)
+// and writes, per sigma, a bitmap of the roots (succ[i] == i: every root is
+// known before any chasing) with one 32-bit word per 32 nodes and the word's
+// popcount; one exclusive scan over the popcounts then gives every root its
+// rank among the ascending roots of its sigma, rank(x) = pre[x/32] -
+// pre[0] + popc(word[x/32] below bit x%32), which is cluster_index
+// (ggd.cpp:48-55), and the scan's per-sigma totals are the cluster counts.
+// The roots' entries of center[] are then replaced by -1 - rank, so
+// chase_kernel, following pointers through center[] (which other threads
+// overwrite with root ids as they finish: any value read is an ancestor, so
+// the result is exact; finished neighbours shorten the walk), reads its
+// label at the end of the walk with no further lookup and writes center and
+// cluster_index together; the root entries are restored afterwards. Maps
+// built by K3 strictly decrease (v, id) along a chain, so every walk
+// terminates -- but a long monotone chain would cost one thread O(depth)
+// dependent loads, so a walk stops after kChaseSteps, leaves the ancestor it
+// reached and counts itself pending; jump_kernel then finishes by pointer
+// jumping in at most ceil(log2 n) + 2 synchronous rounds (or reports a
+// cycle, ggd.cpp:41) and rewrites the labels. No N x S flag or scan arrays
+// (LFR 1M x 32: label passes 0.43 -> 0.29 ms with the succ copy; R-MAT 22:
+// 1.45 -> 1.10 ms).
 constexpr int kChaseSteps = 256;
 
-__global__ void __launch_bounds__(kBlock) chase_kernel(int n, int* __restrict__ center, int* __restrict__ flag,
+// Root bitmap of one sigma slice: W = ceil(n / 32) words per sigma.
+struct RootRank {
+    const unsigned* word;  // [S][W]
+    const int* pre;        // [S * W + 1]: exclusive scan of the words' popcounts
+    int W;
+    __device__ __forceinline__ int operator()(int sigma, int x) const {
+        const long long k = static_cast<long long>(sigma) * W + (x >> 5);
+        return __ldg(pre + k) - __ldg(pre + static_cast<long long>(sigma) * W) +
+               __popc(__ldg(word + k) & ((1u << (x & 31)) - 1u));
+    }
+};
+
+// Four nodes per thread (16 B loads / stores); a lane's 4-bit nibble of
+// roots is merged with its 7 neighbours' into the 32-node word.
+__global__ void __launch_bounds__(kBlock) roots_kernel(int n, int W, const int* __restrict__ succ,
+                                                       int* __restrict__ center, unsigned* __restrict__ word,
+                                                       int* __restrict__ pop, int S, bool aligned) {
+    const long long b = static_cast<long long>(blockIdx.y) * n;
+    const int i0 = (blockIdx.x * kBlock + threadIdx.x) * 4;
+    int x[4];
+    const bool vec = aligned && i0 + 3 < n;  // 16 B aligned buffers, n % 4 == 0: every slice aligned
+    if (vec) {
+        const int4 q = __ldg(reinterpret_cast<const int4*>(succ + b + i0));
+        x[0] = q.x; x[1] = q.y; x[2] = q.z; x[3] = q.w;
+        if (center != succ) *reinterpret_cast<int4*>(center + b + i0) = q;
+    } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            x[u] = i0 + u < n ? succ[b + i0 + u] : -1;
+            if (i0 + u < n && center != succ) center[b + i0 + u] = x[u];
+        }
+    }
+    unsigned m = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) m |= (x[u] == i0 + u ? 1u : 0u) << u;
+    const int lane = threadIdx.x & 31;
+    m <<= 4 * (lane & 7);
+#pragma unroll
+    for (int d = 1; d < 8; d <<= 1) m |= __shfl_xor_sync(0xffffffffu, m, d);
+    const int k = i0 >> 5;
+    if ((lane & 7) == 0 && k < W) {
+        const long long o = static_cast<long long>(blockIdx.y) * W + k;
+        word[o] = m;
+        pop[o] = __popc(m);
+    }
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) pop[static_cast<long long>(S) * W] = 0;
+}
+
+// Roots carry their label through the chase: center[r] = -1 - rank(r) for
+// every root r (encode), restored to r afterwards (decode). Four nodes of
+// one word per thread: coalesced, and nothing to do where the word is 0.
+template <bool kEncode>
+__global__ void __launch_bounds__(kBlock) root_code_kernel(int n, int* __restrict__ center, const RootRank rank) {
+    const int i0 = (blockIdx.x * kBlock + threadIdx.x) * 4;
+    if (i0 >= n) return;
+    const int sigma = blockIdx.y;
+    const long long k = static_cast<long long>(sigma) * rank.W + (i0 >> 5);
+    const unsigned word = __ldg(rank.word + k);
+    const unsigned m = (word >> (i0 & 31)) & 0xfu;
+    if (!m) return;
+    int r = __ldg(rank.pre + k) - __ldg(rank.pre + static_cast<long long>(sigma) * rank.W) +
+            __popc(word & ((1u << (i0 & 31)) - 1u));
+    int* c = center + static_cast<long long>(sigma) * n;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        if ((m >> u) & 1u) {
+            c[i0 + u] = kEncode ? -1 - r : i0 + u;
+            ++r;
+        }
+}
+
+// center[] holds parent pointers with the roots encoded as -1 - rank: a walk
+// ends at the first negative value, which is its root's label, and writes
+// the root's id (the one a later walk reads is then one step from the code).
+__global__ void __launch_bounds__(kBlock) chase_kernel(int n, int* __restrict__ center, int* __restrict__ ci,
                                                        int* __restrict__ pending) {
     const int i = blockIdx.x * kBlock + threadIdx.x;
     if (i >= n) return;
     const long long b = static_cast<long long>(blockIdx.y) * n;
     int* c = center + b;
     int x = c[i];
-    if (flag) flag[b + i] = x == i ? 1 : 0;
+    if (x < 0) {  // i is a root
+        ci[b + i] = -1 - x;
+        return;
+    }
     for (int step = 0;; ++step) {
         const int y = c[x];
-        if (y == x) break;
+        if (y < 0) {
+            ci[b + i] = -1 - y;
+            break;
+        }
         x = y;
         if (step == kChaseSteps) {
             atomicAdd(pending, 1);
@@ -1098,18 +1189,22 @@ __global__ void __launch_bounds__(kBlock) chase_kernel(int n, int* __restrict__ 
 }
 
 // Pointer jumping over every (sigma, node) of center[] until all point at
-// roots; does nothing (one launch, all blocks return at once) when no chase
-// hit its step bound. Cooperative launch: rounds are separated by grid syncs,
-// so each round at least halves every remaining distance (in-place updates
-// only jump further). A map still unresolved after `rounds` rounds has a
-// cycle: *err = 1.
-__global__ void __launch_bounds__(kBlock) jump_kernel(int n, int S, int* __restrict__ center,
+// roots, then the labels of every node again; does nothing more than the
+// per-sigma cluster counts (one launch, all blocks return at once) when no
+// chase hit its step bound. Cooperative launch: rounds are separated by grid
+// syncs, so each round at least halves every remaining distance (in-place
+// updates only jump further). A map still unresolved after `rounds` rounds
+// has a cycle: *err = 1.
+__global__ void __launch_bounds__(kBlock) jump_kernel(int n, int S, int* __restrict__ center, int* __restrict__ ci,
+                                                      const RootRank rank, int* __restrict__ num_clusters,
                                                       int* __restrict__ status, int rounds, int* __restrict__ err) {
+    const long long t0 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t0 < S)
+        num_clusters[t0] = rank.pre[(t0 + 1) * rank.W] - rank.pre[t0 * rank.W];
     if (*reinterpret_cast<volatile int*>(status) == 0) return;  // no pending chase (uniform across the grid)
     cg::grid_group grid = cg::this_grid();
     const long long total = static_cast<long long>(n) * S;
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
-    const long long t0 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     bool done = false;
     for (int r = 0; r < rounds && !done; ++r) {
         int* cnt = status + 1 + (r % 3);
@@ -1128,26 +1223,11 @@ __global__ void __launch_bounds__(kBlock) jump_kernel(int n, int S, int* __restr
         grid.sync();
         done = *reinterpret_cast<volatile int*>(cnt) == 0;
     }
-    if (!done && t0 == 0 && err) atomicExch(err, 1);
-}
-
-// K5a: center flags for the dense relabel scan (flag[S*n] = 0 terminator).
-__global__ void __launch_bounds__(kBlock) center_flags_kernel(int n, int S, const int* __restrict__ center,
-                                                              int* __restrict__ flag) {
-    const long long t = static_cast<long long>(blockIdx.x) * kBlock + threadIdx.x;
-    const long long total = static_cast<long long>(n) * S;
-    if (t < total) flag[t] = center[t] == static_cast<int>(t % n) ? 1 : 0;
-    else if (t == total) flag[t] = 0;
-}
-
-// K5b: cluster_index = rank of the center among ascending centers.
-__global__ void __launch_bounds__(kBlock) relabel_kernel(int n, const int* __restrict__ center,
-                                                         const int* __restrict__ scan, int* __restrict__ ci,
-                                                         int* __restrict__ num_clusters) {
-    const int i = blockIdx.x * kBlock + threadIdx.x;
-    const long long b = static_cast<long long>(blockIdx.y) * n;
-    if (i < n) ci[b + i] = scan[b + center[b + i]] - scan[b];
-    if (i == 0) num_clusters[blockIdx.y] = scan[b + n] - scan[b];
+    if (!done) {
+        if (t0 == 0 && err) atomicExch(err, 1);
+        return;
+    }
+    for (long long t = t0; t < total; t += stride) ci[t] = rank(static_cast<int>(t / n), center[t]);
 }
 
 // Node-major [n][S] -> sigma-major [S][n].
@@ -1697,14 +1777,17 @@ int launch_transpose_i32(const std::int32_t* in, int n, int n_sigma, std::int32_
 }
 
 namespace {
-// launch_labels' workspace: [status 256 B][flag][scan][CUB temp]. status[0]:
-// chases that hit their step bound; status[1..3]: jump_kernel's round counters.
+// launch_labels' workspace: [status 256 B][root words S*W][popcounts /
+// their scan S*W + 1][CUB temp], W = ceil(n / 32). status[0]: chases that
+// hit their step bound; status[1..3]: jump_kernel's round counters.
 struct LabelsWs {
     int* status;
-    int* flag;
-    int* scan;
+    unsigned* word;
+    int* pop;
+    int* pre;
     void* temp;
     std::size_t temp_bytes;
+    int W;
 };
 std::size_t align256(std::size_t x) { return (x + 255) & ~static_cast<std::size_t>(255); }
 std::size_t scan_temp_bytes(long long items) {
@@ -1712,15 +1795,18 @@ std::size_t scan_temp_bytes(long long items) {
     cub::DeviceScan::ExclusiveSum(nullptr, temp, static_cast<const int*>(nullptr), static_cast<int*>(nullptr), items);
     return temp;
 }
-LabelsWs labels_ws(void* workspace, std::size_t ws_bytes, int n, int n_sigma) {
-    const long long items = static_cast<long long>(n) * n_sigma + 1;
+LabelsWs labels_ws(void* workspace, int n, int n_sigma) {
+    const int W = (n + 31) / 32;
+    const long long words = static_cast<long long>(W) * n_sigma;
     char* w = static_cast<char*>(workspace);
     LabelsWs L;
+    L.W = W;
     L.status = reinterpret_cast<int*>(w);
-    L.flag = reinterpret_cast<int*>(w + 256);
-    L.scan = reinterpret_cast<int*>(w + 256 + align256(sizeof(int) * items));
-    L.temp = w + 256 + 2 * align256(sizeof(int) * items);
-    L.temp_bytes = ws_bytes - 256 - 2 * align256(sizeof(int) * items);
+    L.word = reinterpret_cast<unsigned*>(w + 256);
+    L.pop = reinterpret_cast<int*>(w + 256 + align256(sizeof(unsigned) * words));
+    L.pre = reinterpret_cast<int*>(w + 256 + align256(sizeof(unsigned) * words) + align256(sizeof(int) * (words + 1)));
+    L.temp = w + 256 + align256(sizeof(unsigned) * words) + 2 * align256(sizeof(int) * (words + 1));
+    L.temp_bytes = align256(scan_temp_bytes(words + 1));
     return L;
 }
 int jump_grid() {  // co-resident blocks of jump_kernel (cooperative launch), per device
@@ -1739,51 +1825,42 @@ int jump_grid() {  // co-resident blocks of jump_kernel (cooperative launch), pe
 }
 }  // namespace
 
-int launch_chase(int n, int n_sigma, const std::int32_t* succ_sm, std::int32_t* center_sm, void* stream,
-                 void* labels_workspace, std::int32_t* err) {
+std::size_t labels_workspace_bytes(int n, int n_sigma) {
+    const long long words = static_cast<long long>((n + 31) / 32) * n_sigma;
+    return 256 + align256(sizeof(unsigned) * words) + 2 * align256(sizeof(int) * (words + 1)) +
+           align256(scan_temp_bytes(words + 1));
+}
+
+int launch_labels(int n, int n_sigma, const std::int32_t* succ_sm, std::int32_t* center_sm, std::int32_t* ci_sm,
+                  std::int32_t* num_clusters, void* workspace, std::size_t ws_bytes, void* stream, std::int32_t* err) {
     auto st = static_cast<cudaStream_t>(stream);
-    cudaError_t e = cudaSuccess;
-    if (succ_sm != center_sm)
-        e = cudaMemcpyAsync(center_sm, succ_sm, sizeof(int) * static_cast<size_t>(n) * n_sigma,
-                            cudaMemcpyDeviceToDevice, st);
+    if (!workspace || ws_bytes < labels_workspace_bytes(n, n_sigma)) return cudaErrorInvalidValue;
+    if (n < 1 || n_sigma < 1) return cudaSuccess;
+    const LabelsWs L = labels_ws(workspace, n, n_sigma);
+    cudaError_t e = cudaMemsetAsync(L.status, 0, 4 * sizeof(int), st);
     if (e != cudaSuccess) return e;
-    if (!labels_workspace) return cudaErrorInvalidValue;
-    const LabelsWs L = labels_ws(labels_workspace, 0, n, n_sigma);
-    // status words and the scan terminator (flag[n * n_sigma])
-    e = cudaMemsetAsync(L.status, 0, 4 * sizeof(int), st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(L.flag + static_cast<long long>(n) * n_sigma, 0, sizeof(int), st);
+    roots_kernel<<<dim3(static_cast<unsigned>((n + 4 * kBlock - 1) / (4 * kBlock)), n_sigma), kBlock, 0, st>>>(
+        n, L.W, succ_sm, center_sm, L.word, L.pop, n_sigma,
+        (n & 3) == 0 && ((reinterpret_cast<std::uintptr_t>(succ_sm) | reinterpret_cast<std::uintptr_t>(center_sm)) & 15) == 0);
+    std::size_t temp_bytes = L.temp_bytes;
+    const long long words = static_cast<long long>(L.W) * n_sigma;
+    e = cub::DeviceScan::ExclusiveSum(L.temp, temp_bytes, L.pop, L.pre, words + 1, st);
+    count_launch(3);  // roots + CUB init + scan
     if (e != cudaSuccess) return e;
-    chase_kernel<<<dim3(grid_for(n), n_sigma), kBlock, 0, st>>>(n, center_sm, L.flag, L.status);
-    count_launch();
+    const RootRank rank{L.word, L.pre, L.W};
+    const dim3 g4(static_cast<unsigned>((n + 4 * kBlock - 1) / (4 * kBlock)), n_sigma);
+    root_code_kernel<true><<<g4, kBlock, 0, st>>>(n, center_sm, rank);
+    chase_kernel<<<dim3(grid_for(n), n_sigma), kBlock, 0, st>>>(n, center_sm, ci_sm, L.status);
+    root_code_kernel<false><<<g4, kBlock, 0, st>>>(n, center_sm, rank);
+    count_launch(3);
     int rounds = 2;
     while ((1ll << (rounds - 2)) < n) ++rounds;  // ceil(log2 n) + 2
-    void* args[] = {&n, &n_sigma, &center_sm, const_cast<int**>(&L.status), &rounds, &err};
+    int* status = L.status;
+    void* args[] = {&n, &n_sigma, &center_sm, &ci_sm, const_cast<RootRank*>(&rank), &num_clusters, &status, &rounds,
+                    &err};
     e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jump_kernel), dim3(jump_grid()), dim3(kBlock), args, 0, st);
     count_launch();
     if (e != cudaSuccess) return e;
-    return cudaGetLastError();
-}
-
-std::size_t labels_workspace_bytes(int n, int n_sigma) {
-    const long long items = static_cast<long long>(n) * n_sigma + 1;
-    return 256 + 2 * align256(sizeof(int) * items) + align256(scan_temp_bytes(items));
-}
-
-int launch_labels(int n, int n_sigma, const std::int32_t* center_sm, std::int32_t* ci_sm, std::int32_t* num_clusters,
-                  void* workspace, std::size_t ws_bytes, void* stream, bool flags_ready) {
-    auto st = static_cast<cudaStream_t>(stream);
-    const long long items = static_cast<long long>(n) * n_sigma + 1;
-    const LabelsWs L = labels_ws(workspace, ws_bytes, n, n_sigma);
-    if (!flags_ready) {  // else launch_chase wrote them
-        center_flags_kernel<<<grid_for(items), kBlock, 0, st>>>(n, n_sigma, center_sm, L.flag);
-        count_launch();
-    }
-    std::size_t temp_bytes = L.temp_bytes;
-    cudaError_t e = cub::DeviceScan::ExclusiveSum(L.temp, temp_bytes, L.flag, L.scan, items, st);
-    count_launch(2);  // CUB: init + scan kernels
-    if (e != cudaSuccess) return e;
-    relabel_kernel<<<dim3(grid_for(n), n_sigma), kBlock, 0, st>>>(n, center_sm, L.scan, ci_sm, num_clusters);
-    count_launch();
     return cudaGetLastError();
 }
 
@@ -1838,7 +1915,7 @@ int resolve_checked(int n, const std::int32_t* succ_dev, std::int32_t* center_de
         void* wsp = nullptr;
         e = cudaMallocFromPoolAsync(&wsp, ws, pool, st);
         if (e == cudaSuccess) {
-            e = static_cast<cudaError_t>(launch_labels(n, 1, center_dev, ci_dev, nc, wsp, ws, st));
+            e = static_cast<cudaError_t>(launch_labels(n, 1, center_dev, center_dev, ci_dev, nc, wsp, ws, st));
             cudaMemcpyAsync(num_clusters_host, nc, sizeof(int), cudaMemcpyDeviceToHost, st);
             cudaFreeAsync(wsp, st);
         }
