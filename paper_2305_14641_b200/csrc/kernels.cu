@@ -167,15 +167,20 @@ __global__ void hub_split_kernel(const int* __restrict__ deg_sorted, int rows, l
 constexpr int kRowsPerGrab = 2;
 constexpr int kHeavyDegree = 256;  // GGD argmin: rows above this degree use a block each
 
+// Sort keys of the longest-first schedule: the degree capped at 2^bits - 1
+// (bits = 24 where the hub split compares degrees; 11 for the unit-weight
+// fast-forward, whose order only needs "long rows first": 2 radix passes
+// instead of 4), and under the polled upload the slab above it.
 __global__ void row_degree_kernel(const long long* __restrict__ off, int row_begin, int rows, int* __restrict__ deg,
-                                  int* __restrict__ id, const int* __restrict__ slab_flags, int b1, int b2, int b3) {
+                                  int* __restrict__ id, const int* __restrict__ slab_flags, int b1, int b2, int b3,
+                                  int bits) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= rows) return;
     const int i = row_begin + k;
-    deg[k] = static_cast<int>(off[i + 1] - off[i]);
+    deg[k] = min(static_cast<int>(min(off[i + 1] - off[i], 0x7fffffffll)), (1 << bits) - 1);
     if (slab_flags) {  // polled upload: slab-major (earlier slabs first), heaviest first inside a slab
         const int slab = (i >= b1) + (i >= b2) + (i >= b3);
-        deg[k] = ((3 - slab) << 24) | min(deg[k], (1 << 24) - 1);
+        deg[k] |= (3 - slab) << bits;
     }
     id[k] = i;
 }
@@ -1370,11 +1375,17 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
         int* id_out = reinterpret_cast<int*>(b + 3 * arr);
         int* counter = reinterpret_cast<int*>(b + 4 * arr);
         void* temp = b + 4 * arr + 256;
+        // hub rows (see hub_split_kernel) need the degree itself; otherwise
+        // capped keys (11 bits + 2 slab bits) sort in 2 passes
+        const bool hubs = !(ff && p.weight_mode == kUnit);
+        const int key_bits = hubs ? 24 : 11;
         row_degree_kernel<<<grid_for(rows), kBlock, 0, st>>>(reinterpret_cast<const long long*>(p.offsets),
                                                               p.row_begin, rows, deg_in, id_in, p.slab_flags,
-                                                              p.slab_bound[1], p.slab_bound[2], p.slab_bound[3]);
+                                                              p.slab_bound[1], p.slab_bound[2], p.slab_bound[3],
+                                                              key_bits);
         count_launch();
-        e = cub::DeviceRadixSort::SortPairsDescending(temp, sort_bytes, deg_in, deg_out, id_in, id_out, rows, 0, 32, st);
+        e = cub::DeviceRadixSort::SortPairsDescending(temp, sort_bytes, deg_in, deg_out, id_in, id_out, rows, 0,
+                                                      key_bits + 2, st);
         count_launch(2);
         if (e != cudaSuccess) {  // no scratch leaks on the error path
             cudaFreeAsync(sched, st);
@@ -1387,10 +1398,9 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
         // an SM of its own there.
         int* hub_count = counter + 1;
         int* hub_counter = counter + 2;
-        const bool hubs = !(ff && p.weight_mode == kUnit);
         const long long threshold = hubs ? std::max<long long>(4096, p.nnz / 4096) : (1ll << 62);
-        hub_split_kernel<<<1, 1, 0, st>>>(deg_out, rows, threshold, p.slab_flags ? 0xffffff : -1, hub_count, counter,
-                                          hub_counter);
+        hub_split_kernel<<<1, 1, 0, st>>>(deg_out, rows, threshold, p.slab_flags ? (1 << key_bits) - 1 : -1, hub_count,
+                                          counter, hub_counter);
         count_launch();
         const RowSched R{id_out, counter, nullptr};
         const RowSched Rh{id_out, hub_counter, hub_count};
@@ -1457,7 +1467,8 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
             int* id_in = reinterpret_cast<int*>(b + 2 * arr);
             int* id_out = reinterpret_cast<int*>(b + 3 * arr);
             row_degree_kernel<<<grid_for(rows), kBlock, 0, st>>>(reinterpret_cast<const long long*>(p.offsets),
-                                                                  p.row_begin, rows, deg_in, id_in, nullptr, 0, 0, 0);
+                                                                  p.row_begin, rows, deg_in, id_in, nullptr, 0, 0, 0,
+                                                                  24);
             e = cub::DeviceRadixSort::SortPairsDescending(b + 4 * arr, sort_bytes, deg_in, deg_out, id_in, id_out, rows,
                                                           0, 32, st);
             count_launch(3);
