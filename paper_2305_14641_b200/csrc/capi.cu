@@ -991,11 +991,13 @@ static void cluster_sweep_impl(const gqc_csr* g, const double* sigmas, int32_t n
         };
         ClassOrderScope order;
         make_class_order(C, d, v_nm, n_sigma, n_sigma, st, order);
+        // the degree sample reads the host CSR while the potentials run
+        const int sub = light_row_sigmas_host(g->offsets, n);
         for (std::size_t q = 0; q + 1 < cuts.size(); ++q) {
             const int s0 = cuts[q], Sc = cuts[q + 1] - cuts[q];
             const std::size_t o = static_cast<std::size_t>(s0) * n;
             cuda_check(launch_successors(n, d.offsets, d.nbr, v_nm, n_sigma, s0, Sc, 0, n, ds + o, 1, n, nnz, C.pool, st,
-                                         order.get()),
+                                         order.get(), sub),
                        "successor kernel");
             cuda_check(launch_labels(n, Sc, ds + o, dc + o, dci + o, dnc + s0, ws, wsb, st, d_err), "label kernels");
             if (intra_out)
@@ -1183,6 +1185,7 @@ static void sweep_multi_impl(const gqc_csr* g, const double* sigmas, int S, cons
     }
 
     // GGD of every sigma chunk on its owner once all potentials are in
+    int sub_multi = 0;
     for (int q = 0; q < nchunks; ++q) {
         const int d = devices[q], Sq = s_count(q), s0 = s_begin(q);
         DeviceCtx& X = *C[d];
@@ -1206,8 +1209,9 @@ static void sweep_multi_impl(const gqc_csr* g, const double* sigmas, int S, cons
         void* ws = Bq.ws.get<char>(wsb);
         ClassOrderScope order;
         make_class_order(X, dg, V[q], chunk, Sq, st, order);
+        if (sub_multi == 0) sub_multi = light_row_sigmas_host(g->offsets, n);  // while the potentials run
         cuda_check(launch_successors(n, dg.offsets, dg.nbr, V[q], chunk, 0, Sq, 0, n, ds, 1, n, nnz, X.pool, st,
-                                     order.get()),
+                                     order.get(), sub_multi),
                    "successor kernel");
         int* d_err = ggd_err_word(Bq.err, Bq.err_host, st);
         cuda_check(launch_labels(n, Sq, ds, dc, dci, dnc, ws, wsb, st, d_err), "label kernels");
@@ -1473,7 +1477,7 @@ gqc_status gqc_dev_ggd(const gqc_csr* g, const double* v, int32_t n_sigma, int32
         ClassOrderScope order;
         make_class_order(C, *g, v, n_sigma, n_sigma, st, order);
         cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, 0, g->n, s, 1, g->n, g->nnz, C.pool,
-                                     st, order.get()),
+                                     st, order.get(), light_row_sigmas_device(g->offsets, g->n, g->nnz, st)),
                    "successor kernel");
         cuda_check(launch_labels(g->n, n_sigma, s, center, cluster_index, num_clusters, workspace, workspace_bytes, st),
                    "label kernels");
@@ -1492,7 +1496,8 @@ gqc_status gqc_dev_successors(const gqc_csr* g, const double* v, int32_t n_sigma
         ClassOrderScope order;
         make_class_order(C, *g, v, n_sigma, n_sigma, st, order);
         cuda_check(launch_successors(g->n, g->offsets, g->nbr, v, n_sigma, 0, n_sigma, row_begin, row_end, succ_rows,
-                                     n_sigma, 1, g->nnz, C.pool, st, order.get()),
+                                     n_sigma, 1, g->nnz, C.pool, st, order.get(),
+                                     light_row_sigmas_device(g->offsets, g->n, g->nnz, st)),
                    "successor kernel");
     });
 }

@@ -105,10 +105,19 @@ int launch_class_order(std::int32_t n, const std::int64_t* offsets, long long nn
 // (sigma-major: out_row = 1, out_col = n; node-major shard: out_row = ld, out_col = 1).
 // co (optional): the field's class order; sigmas with dir != 0 take the
 // fast path (only best-class neighbours' potentials are gathered).
+// sub: sigmas per light-row launch (32, or 16 for graphs made mostly of rows
+// with a handful of neighbours: two rows per warp), see light_row_sigmas_*.
 int launch_successors(std::int32_t n, const std::int64_t* offsets, const std::int32_t* nbr, const double* v,
                       std::int32_t ld, std::int32_t s0, std::int32_t n_sigma, std::int32_t row_begin,
                       std::int32_t row_end, std::int32_t* out, long long out_row, long long out_col, long long nnz,
-                      void* pool, void* stream, const ClassOrder* co = nullptr);
+                      void* pool, void* stream, const ClassOrder* co = nullptr, int sub = 32);
+// The GGD argmin's light-row launch width for a CSR from a sample of 8192
+// pseudo-random rows' degrees: 16 when more than 20% have <= 4 neighbours,
+// else 32. Host offsets, or device offsets (cached per device and CSR
+// pointer / shape: one stream synchronisation the first time; only the
+// speed depends on it).
+int light_row_sigmas_host(const std::int64_t* offsets, std::int32_t n);
+int light_row_sigmas_device(const std::int64_t* offsets, std::int32_t n, long long nnz, void* stream);
 // out[s] = CSR entries (i, j) whose cluster_index matches for sigma s (device,
 // sigma-major labels [n_sigma][n]); the unit-weight modularity intra term.
 int launch_intra_counts(std::int32_t n, std::int32_t n_sigma, const std::int64_t* offsets, const std::int32_t* nbr,

@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <atomic>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -1698,9 +1699,71 @@ int launch_intra_counts(int n, int n_sigma, const std::int64_t* offsets, const s
     return cudaGetLastError();
 }
 
+namespace {
+// Degree sample of the GGD argmin's launch shape: kTinySample pseudo-random
+// rows (multiplicative hashing: evenly spaced ids would follow R-MAT's id
+// structure, where ids with many trailing zero bits are hubs).
+constexpr int kTinySample = 8192;
+constexpr int kTinyRowDegree = 4;
+__host__ __device__ inline long long sample_row(int k, long long n) {
+    unsigned long long h = static_cast<unsigned long long>(k) * 0x9E3779B97F4A7C15ull;
+    h ^= h >> 29;
+    return static_cast<long long>(h % static_cast<unsigned long long>(n));
+}
+__global__ void tiny_sample_kernel(const long long* __restrict__ off, int n, int* __restrict__ count) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool tiny = k < kTinySample && off[sample_row(k, n) + 1] - off[sample_row(k, n)] <= kTinyRowDegree;
+    const unsigned m = __ballot_sync(0xffffffffu, tiny);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(count, __popc(m));
+}
+int sub_from_count(int tiny) { return 5 * tiny > kTinySample ? 16 : 32; }  // > 20% of rows tiny
+}  // namespace
+
+int light_row_sigmas_host(const std::int64_t* offsets, int n) {
+    if (n < 1) return 32;
+    int tiny = 0;
+    for (int k = 0; k < kTinySample; ++k) {
+        const long long i = sample_row(k, n);
+        tiny += offsets[i + 1] - offsets[i] <= kTinyRowDegree;
+    }
+    return sub_from_count(tiny);
+}
+
+int light_row_sigmas_device(const std::int64_t* offsets, int n, long long nnz, void* stream) {
+    if (n < 1) return 32;
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, int, long long>, int> cache;  // per device, CSR shape
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_tuple(dev, static_cast<const void*>(offsets), n, nnz);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    auto st = static_cast<cudaStream_t>(stream);
+    int* d = nullptr;
+    int h = 0;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(int), st) != cudaSuccess) {
+        cudaGetLastError();
+        return 32;
+    }
+    cudaMemsetAsync(d, 0, sizeof(int), st);
+    tiny_sample_kernel<<<kTinySample / kBlock, kBlock, 0, st>>>(reinterpret_cast<const long long*>(offsets), n, d);
+    count_launch();
+    cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(d, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return 32;
+    const int sub = sub_from_count(h);
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = sub;
+    return sub;
+}
+
 int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nbr, const double* v, int ld, int s0,
                       int n_sigma, int row_begin, int row_end, std::int32_t* out, long long out_row, long long out_col,
-                      long long nnz, void* pool, void* stream, const ClassOrder* co) {
+                      long long nnz, void* pool, void* stream, const ClassOrder* co, int sub) {
+    if (sub < 1 || sub > 32) sub = kSuccSub;
     (void)n;
     auto st = static_cast<cudaStream_t>(stream);
     auto off = reinterpret_cast<const long long*>(offsets);
@@ -1740,12 +1803,14 @@ int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nb
         // light rows: the kernels index threads in 32 bits, so the row range
         // goes in sub-launches of fewer than 2^31 threads (graphs of ~67M+
         // nodes at 32 sigmas), each with its output moved to its first row.
-        // GQC_SUCC_SUB < 32 runs the plain argmin in launches of that many
-        // sigmas over all rows, so each launch gathers one slice of every
-        // node's V line (8 sigmas: 64 MB at LFR 1M, L2-sized). Measured (32
-        // sigmas, GGD ms, 32 / 8 / 4 per launch): LFR 1M 1.33 / 1.87 / 2.58,
-        // R-MAT 22 6.06 / 5.00 / 6.13 — rows of several degrees per warp cost
-        // LFR more than the L2 reuse saves, so one launch stays the default.
+        // sub < 32 runs the plain argmin in launches of that many sigmas
+        // over all rows (a warp then takes 32 / sub rows), so each launch
+        // gathers one slice of every node's V line. Measured (32 sigmas, GGD
+        // ms, 32 / 16 / 8 / 4 per launch): LFR 1M 1.33 / 1.43 / 1.87 / 2.58,
+        // R-MAT 22 5.94 / 4.52 / 5.00 / 6.13: graphs made mostly of rows
+        // with a handful of neighbours (R-MAT: 79% of rows have <= 4) gain
+        // from two rows per warp, the others do not; the callers pick it
+        // from a degree sample (light_row_sigmas).
         const long long per = ((1ll << 31) - 2 * kBlock) / 32;
         for (long long r0 = 0; r0 < rows; r0 += per) {
             const int rr = static_cast<int>(std::min<long long>(per, rows - r0));
@@ -1757,8 +1822,8 @@ int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nb
                 count_launch();
             } else {  // rows of more than kTinyDegree neighbours (tiny ones: successors_tiny_kernel)
                 const int lo = tiny_rows ? kTinyDegree + 1 : 0;
-                for (int q0 = 0; q0 < Sc; q0 += kSuccSub) {
-                    const int Sq = std::min(kSuccSub, Sc - q0);
+                for (int q0 = 0; q0 < Sc; q0 += sub) {
+                    const int Sq = std::min(sub, Sc - q0);
                     const SuccOut Or{O.out + r0 * out_row + q0 * out_col, out_row, out_col};
                     successors_kernel<<<grid_for(static_cast<long long>(rr) * Sq), kBlock, 0, st>>>(
                         off, nbr, v, ld, s0 + c0 + q0, Sq, rb, rr, Or, lo, kHeavyDegree);
