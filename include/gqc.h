@@ -293,6 +293,14 @@ gqc_status gqc_dev_transpose(const double* v_nm, int32_t n, int32_t n_sigma, dou
  * NULL on failure. */
 void* gqc_host_alloc(size_t bytes);
 void gqc_host_free(void* p);
+/* Optional: size the context buffers of GQC_OPT_DEVICE for host-API sweeps
+ * (gqc_cluster_sweep and friends) of graphs up to n nodes / nnz CSR entries
+ * and n_sigma sigmas per call, and grow its stream-ordered scratch pool, so
+ * the first call of a process does not allocate device memory on its
+ * critical path (the CLI runs it on its device warm-up thread once the graph
+ * is loaded). Later calls that need more still grow the buffers. */
+gqc_status gqc_reserve(int32_t n, int64_t nnz, int32_t n_sigma);
+
 /* Page-lock an existing host range (cudaHostRegister) / release it: a CSR
  * the caller keeps across calls then uploads at PCIe speed, under the
  * potential launch (the CLI registers its graph while it reads the labels). */

@@ -682,6 +682,38 @@ gqc_status gqc_init(void) {
     });
 }
 
+gqc_status gqc_reserve(int32_t n, int64_t nnz, int32_t n_sigma) {
+    return guarded([&] {
+        if (n < 1 || nnz < 0 || n_sigma < 1) fail(GQC_EINVAL, "bad reserve sizes");
+        DeviceCtx& C = ctx();
+        const std::size_t cells = static_cast<std::size_t>(n) * n_sigma;
+        C.off.get<std::int64_t>(static_cast<std::size_t>(n) + 1);
+        C.nbr.get<std::int32_t>(std::max<std::int64_t>(nnz, 1));
+        C.v_nm.get<double>(cells);
+        C.succ.get<int>(cells);
+        C.center.get<int>(cells);
+        C.ci.get<int>(cells);
+        C.nc.get<int>(n_sigma);
+        C.intra.get<long long>(n_sigma);
+        C.ws.get<char>(labels_workspace_bytes(n, n_sigma));
+        C.slab_sync.get<int>(8);
+        if (!C.slab_host) {
+            cuda_check(cudaHostAlloc(&C.slab_host, 8 * sizeof(int), cudaHostAllocDefault), "cudaHostAlloc");
+            for (int k = 0; k < 8; ++k) C.slab_host[k] = 1;
+        }
+        pinned_counts(C, n_sigma);
+        (void)ggd_err_word(C.err, C.err_host, C.stream);
+        // the pool keeps what it has held (release threshold: never): one
+        // block the size of a sweep's stream-ordered scratch (schedule arrays
+        // and sort, prefix tables, argmin lists), handed back at once
+        void* p = nullptr;
+        const std::size_t est = 20 * static_cast<std::size_t>(n) + (static_cast<std::size_t>(nnz) / 64) + (64u << 20);
+        cuda_check(cudaMallocFromPoolAsync(&p, est, C.pool, C.stream), "pool reserve");
+        cuda_check(cudaFreeAsync(p, C.stream), "pool reserve");
+        cuda_check(cudaStreamSynchronize(C.stream), "sync");
+    });
+}
+
 gqc_status gqc_set_option(gqc_option key, int64_t value) {
     return guarded([&] {
         if (key == GQC_OPT_EXP_MODE) {

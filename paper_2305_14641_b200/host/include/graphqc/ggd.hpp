@@ -41,6 +41,12 @@ std::vector<ClusterAssignment> cluster_batch(const Graph& g, std::span<const dou
 void set_max_gpus(int gpus);
 int max_gpus();
 
+// Optional, not a reference function: sizes the device buffers and the
+// pinned label staging for cluster / cluster_batch calls on g with up to
+// n_sigma sigmas (gqc_reserve), so the first call of a process does not
+// allocate on its critical path. The CLI runs it on its warm-up thread.
+void reserve_for(const Graph& g, int n_sigma, bool with_center);
+
 namespace detail {
 // cluster_batch plus modularity's intra-cluster weight per sigma, counted
 // exactly on the device with the labels (unit-weight graphs; empty

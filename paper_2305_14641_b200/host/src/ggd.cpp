@@ -149,6 +149,15 @@ std::vector<ClusterAssignment> cluster_batch_intra(const Graph& g, std::span<con
 
 }  // namespace detail
 
+void reserve_for(const Graph& g, int n_sigma, bool with_center) {
+    if (n_sigma < 1) throw std::invalid_argument("sigma count must be at least 1");
+    const int m = std::min(n_sigma, 64);  // cluster_batch_intra's chunk
+    const std::size_t n = static_cast<std::size_t>(g.num_nodes());
+    detail::check(gqc_reserve(g.num_nodes(), 2 * g.num_edges(), m));
+    detail::PinnedStage stage;
+    (void)stage.get(static_cast<std::size_t>(m) * n * (with_center ? 2 : 1));
+}
+
 std::vector<ClusterAssignment> cluster_batch(const Graph& g, std::span<const double> sigmas, bool with_center,
                                              int workers) {
     return detail::cluster_batch_intra(g, sigmas, with_center, workers, nullptr);

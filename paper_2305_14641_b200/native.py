@@ -95,6 +95,7 @@ def _load():
         "gqc_dev_transpose": [P, i32, i32, P, P],
         "gqc_dev_successors": [P, P, i32, i32, i32, P, P],
         "gqc_dev_resolve": [i32, i32, P, P, P, P, P, C.c_size_t, P],
+        "gqc_reserve": [i32, i64, i32],
     }.items():
         fn = getattr(lib, name)
         fn.argtypes = args
@@ -232,6 +233,12 @@ def get_options():
 
 def device_count() -> int:
     return int(_lib.gqc_device_count())
+
+
+def reserve(n: int, nnz: int, n_sigma: int):
+    """gqc_reserve: size the device context's buffers for host-API sweeps of
+    graphs up to n nodes / nnz entries / n_sigma sigmas per call."""
+    _check(_lib.gqc_reserve(int(n), int(nnz), int(n_sigma)))
 
 
 def last_launch_count() -> int:

@@ -714,3 +714,19 @@ def test_cluster_sweep_intra_counts():
     w = H.random_graph(300, 5, 3, unit=False)
     with pytest.raises(ValueError, match="intra counts need unit weights"):
         N.cluster_sweep_intra(w.csr(N), [1.0])
+
+
+def test_reserve_then_sweep_same_bits():
+    """gqc_reserve sizes the context buffers ahead of a host-API sweep (the
+    CLI's warm-up thread): the sweep that follows gives the same bits as one
+    without it; bad sizes are GQC_EINVAL."""
+    g = H.random_graph(3001, 9, 31, unit=True)
+    sig = O.log_sigma_grid(10.0, 16)
+    res0, v0, _ = N.cluster_sweep(g.csr(N), sig, want_v=True)
+    N.reserve(4000, 2 * 20000, 16)
+    res1, v1, _ = N.cluster_sweep(g.csr(N), sig, want_v=True)
+    assert np.array_equal(v0.view(np.int64), v1.view(np.int64))
+    assert all(np.array_equal(a.cluster_index, b.cluster_index) for a, b in zip(res0, res1))
+    for bad in [(0, 10, 1), (10, -1, 1), (10, 10, 0)]:
+        with pytest.raises(ValueError):
+            N.reserve(*bad)
