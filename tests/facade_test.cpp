@@ -3,7 +3,11 @@
 // metrics_test.cpp, sweep_test.cpp in the reference) that do not need a
 // potential field. Built and run by tests/test_facade.py.
 #include <cmath>
+#include <cstdint>
 #include <iostream>
+#include <map>
+#include <random>
+#include <vector>
 #include <sstream>
 #include <string>
 #include <tuple>
@@ -54,8 +58,57 @@ static std::string what_of(const std::string& text) {
     return "";
 }
 
+// graph.cpp:25-71 restated the slow way (a std::map per row, keep-first
+// collapse in input order): the CSR the facade's multi-threaded host build
+// must reproduce byte for byte.
+static bool csr_matches_map_build(std::int32_t n, const std::vector<Edge>& edges) {
+    std::vector<std::map<std::int32_t, double>> rows(n);
+    for (const Edge& e : edges) {
+        if (e.u == e.v) continue;
+        if (rows[e.u].count(e.v)) continue;  // keep-first
+        rows[e.u][e.v] = e.weight;
+        rows[e.v][e.u] = e.weight;
+    }
+    Graph g(n, std::span<const Edge>(edges), 10.0);
+    const Graph::CsrView c = g.csr();
+    std::int64_t k = 0;
+    bool unit = true;
+    for (std::int32_t i = 0; i < n; ++i) {
+        if (c.offsets[i] != k) return false;
+        for (const auto& [j, w] : rows[i]) {
+            if (c.nbr[k] != j || c.weights[k] != w) return false;
+            unit = unit && w == 1.0;
+            ++k;
+        }
+    }
+    return c.offsets[n] == k && c.unit == unit;
+}
+
 int main(int argc, char** argv) {
     const std::string data = argc > 1 ? argv[1] : "tests/golden";
+    // the host CSR build with many threads (>= 2^18 edges): random weighted
+    // edges with duplicates in both orientations (some with another weight)
+    // and self loops, and a unit-weight variant
+    {
+        std::mt19937_64 rng(7);
+        const std::int32_t n = 50000;
+        const std::size_t m = 400000;
+        std::vector<Edge> e(m);
+        const double ws[4] = {0.5, 1.0, 1.5, 2.0};
+        for (auto& x : e) x = {static_cast<std::int32_t>(rng() % n), static_cast<std::int32_t>(rng() % n), ws[rng() % 4]};
+        for (std::size_t q = 0; q < m / 20; ++q) {  // re-emit earlier pairs
+            const Edge& s = e[rng() % m];
+            Edge& d = e[rng() % m];
+            d = (rng() & 1) ? Edge{s.v, s.u, ws[rng() % 4]} : Edge{s.u, s.v, s.weight};
+        }
+        for (std::size_t q = 0; q < m / 100; ++q) {  // self loops
+            Edge& x = e[rng() % m];
+            x.v = x.u;
+        }
+        CHECK(csr_matches_map_build(n, e));
+        for (auto& x : e) x.weight = 1.0;
+        CHECK(csr_matches_map_build(n, e));
+    }
     // graph_test.cpp: parsing builds a symmetric unit-weight graph
     {
         Graph g = from_text("a b\nb c\n");

@@ -265,7 +265,7 @@ def test_cluster_hop_cap_extension(tmp_path):
     assert code == 0 and out.splitlines()[1] == README_ROW
 
 
-@pytest.mark.parametrize("kind", ["int", "mixed", "sparse", "error"])
+@pytest.mark.parametrize("kind", ["int", "mixed", "sparse", "error", "weighted_dups"])
 def test_large_edge_files_ingest_like_the_reference(tmp_path, kind):
     """Multi-chunk (> 1 MB) edge files through the parallel loader's paths:
     compact integer names, a non-integer name deep in the file (chunks
@@ -274,12 +274,25 @@ def test_large_edge_files_ingest_like_the_reference(tmp_path, kind):
     --graph` (modularity of a labelling over the loaded graph) against the
     reference's own loader and metrics (oracle/_ref), or the oracle."""
     from oracle import pyref as R
-    rng = np.random.default_rng({"int": 1, "mixed": 2, "sparse": 3, "error": 4}[kind])
-    n, m = 30000, 120000
+    rng = np.random.default_rng({"int": 1, "mixed": 2, "sparse": 3, "error": 4, "weighted_dups": 5}[kind])
+    n, m = (30000, 120000) if kind != "weighted_dups" else (60000, 400000)
     u = rng.integers(0, n, m)
     v = rng.integers(0, n, m)
     name = (lambda x: str(x * 70001 + 12345678)) if kind == "sparse" else str
-    lines = [f"{name(a)} {name(b)}\n" for a, b in zip(u, v)]
+    if kind == "weighted_dups":
+        # > 2^18 edges: the host CSR build's multi-threaded counting sorts,
+        # with duplicates in both orientations (some with another weight: the
+        # first is kept, a warning names it) and self loops (dropped)
+        k = m // 20
+        src, at = rng.integers(0, m, k), rng.integers(0, m, k)
+        flip = rng.random(k) < 0.5
+        u[at], v[at] = np.where(flip, v[src], u[src]), np.where(flip, u[src], v[src])
+        loops = rng.integers(0, m, m // 100)
+        v[loops] = u[loops]
+        w = rng.choice([0.5, 1.0, 1.5, 2.0], m)
+        lines = [f"{a} {b} {x}\n" for a, b, x in zip(u, v, w)]
+    else:
+        lines = [f"{name(a)} {name(b)}\n" for a, b in zip(u, v)]
     if kind == "mixed":
         lines[m * 3 // 4] = "node_x 17\n"
     if kind == "error":
@@ -294,12 +307,14 @@ def test_large_edge_files_ingest_like_the_reference(tmp_path, kind):
     # labels: one class per node in first-appearance order, three classes
     seen = {}
     for ln in lines:
-        for t in ln.split():
+        for t in ln.split()[:2]:
             seen.setdefault(t, len(seen))
     lab = {t: (k * 7) % 3 for t, k in seen.items()}
     lpath = write(tmp_path / "l.labels", "".join(f"{t} {c}\n" for t, c in lab.items()))
     code, out, err = run("eval", lpath, lpath, "--graph", gpath)
     assert code == 0, err
+    if kind == "weighted_dups":
+        assert "warning: duplicate edge" in err
     if not R.available():
         return
     g = R.Graph.load(gpath)
