@@ -489,6 +489,9 @@ void run_potentials(DeviceCtx& C, const gqc_csr& g, const double* sigmas, int S,
         }
         if (!weighted) {
             P.weight_mode = kUnit;
+            // graphs with isolated rows (degree sample, cached per device CSR)
+            // take the fast-forward's isolated-row instantiation
+            if (t_opt.kernel == GQC_KERNEL_FASTFWD) P.iso = isolated_rows_device(g.offsets, g.n, g.nnz, st);
         } else if (mode == GQC_EXP_EIGEN) {
             P.weight_mode = kDevicePexp;
             if (tail && last_deg > 0) {

@@ -64,6 +64,7 @@ struct PotentialLaunch {
     // [slab_bound[k], slab_bound[k+1]) may be read once slab_flags[k] != 0
     // (set by a copy after the slab's data on the copy stream); rows are
     // scheduled slab-major. slab_err: set if a flag never arrives (timeout).
+    int iso;  // the graph has isolated rows (degree sample): the fast-forward's isolated-row instantiation
     const int* slab_flags;
     std::int32_t slab_bound[5];
     int* slab_err;
@@ -118,6 +119,10 @@ int launch_successors(std::int32_t n, const std::int64_t* offsets, const std::in
 // speed depends on it).
 int light_row_sigmas_host(const std::int64_t* offsets, std::int32_t n);
 int light_row_sigmas_device(const std::int64_t* offsets, std::int32_t n, long long nnz, void* stream);
+// 1 when more than 1% of the same sample of a device CSR's rows are isolated
+// (no neighbours): the unit-weight fast-forward then runs the instantiation
+// with the isolated-row shortcut.
+int isolated_rows_device(const std::int64_t* offsets, std::int32_t n, long long nnz, void* stream);
 // out[s] = CSR entries (i, j) whose cluster_index matches for sigma s (device,
 // sigma-major labels [n_sigma][n]); the unit-weight modularity intra term.
 int launch_intra_counts(std::int32_t n, std::int32_t n_sigma, const std::int64_t* offsets, const std::int32_t* nbr,

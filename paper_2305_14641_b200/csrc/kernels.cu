@@ -134,6 +134,11 @@ struct PrefixTable {
     int* count;
     int* t_end;
     double* s_end;
+    // numerator of an isolated row (no neighbours): its own column adds 0,
+    // so it is n - 1 pure adds of pW (iso_last, also the row n - 1 under a
+    // tail) or, under an odd-n tail, n - 2 pure adds then the tail constant
+    double* iso;
+    double* iso_last;
 };
 
 // Longest-first dynamic row scheduling of the warp kernel: rows in
@@ -193,6 +198,17 @@ __global__ void prefix_kernel(const __grid_constant__ PotentialLaunch P, PrefixT
     const double cst = (q & 1) ? c.eW : c.pW;
     build_prefix(cst, P.n, T.t + q * kPrefixCap, T.s0 + q * kPrefixCap, T.inc + q * kPrefixCap, T.count + q,
                  T.t_end + q, T.s_end + q);
+    if (q & 1) return;
+    auto pure = [&](const int L) {  // L pure adds of pW from 0
+        if (L <= 0) return 0.0;
+        if (L < T.t_end[q])
+            return prefix_value(T.t + q * kPrefixCap, T.s0 + q * kPrefixCap, T.inc + q * kPrefixCap, T.count[q], L);
+        Chain ch = make_chain(T.s_end[q], cst);
+        ff_run(ch, cst, L - T.t_end[q]);
+        return ch.s;
+    };
+    T.iso_last[q >> 1] = pure(P.n - 1);
+    T.iso[q >> 1] = P.tail ? __dadd_rn(pure(P.n - 2), c.pWt) : T.iso_last[q >> 1];
 }
 
 // Value of the first run (L pure adds from 0) for chain q, then the chain's
@@ -412,7 +428,11 @@ __device__ __forceinline__ int load_nbr(const PotentialLaunch& P, const long lon
 // row-range launches, i.e. shards of a multi-device sweep, where the longest
 // row is the critical path; a whole-graph launch keeps the chunked walk, which
 // measured faster for throughput and does not carry the extra code).
-template <bool kFF, int kW, bool kLong = false>
+// kIso: isolated rows take a shortcut (their numerator is a per-sigma
+// constant, only the denominator is walked); a separate instantiation,
+// chosen from the degree sample, because the branch costs the other rows
+// registers (LFR 4.451 -> 4.474 ms with it compiled in).
+template <bool kFF, int kW, bool kLong = false, bool kIso = false>
 __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp_kernel(const __grid_constant__ PotentialLaunch P,
                                                                 const PrefixTable T, const RowSched R) {
     __shared__ double sc[kSigmaFields][kMaxSigmaPerLaunch];
@@ -528,6 +548,27 @@ __global__ void __launch_bounds__(kBlock, kWarpKernelBlocksPerSM) potential_warp
         Chain num, den;
         num.s = 0.0; num.top = 0.0; num.inc = 0.0; num.f_tie = tie_num; num.flags = 0;
         den.s = 0.0; den.top = 0.0; den.inc = 0.0; den.f_tie = tie_den; den.flags = 0;
+        if constexpr (kFF && kW == kUnit && kIso) {
+            if (kbeg == kend) {  // isolated row: the numerator is a per-sigma constant
+                if (i > 0) w_run(num, den, 0, i);  // (the numerator's prefix is unused)
+                den.s = __dadd_rn(den.s, 1.0);
+                const int L = n - 1 - i;  // columns after the row's own
+                if (L > 0) {
+                    den.top = 0.0;
+                    if (tail) {
+                        ff_run(den, eW, L - 1);
+                        den.s = __dadd_rn(den.s, sc[6][s]);
+                    } else {
+                        ff_run(den, eW, L);
+                    }
+                }
+                const double nv = (tail && i == n - 1) ? T.iso_last[s] : T.iso[s];
+                if (lane < S)
+                    lane_out[static_cast<long long>(i - P.row_begin) * P.out_ld] =
+                        __dmul_rn(sc[0][s], __ddiv_rn(nv, den.s));
+                continue;
+            }
+        }
         int pos = 0;              // first column not yet added
         bool self_pending = true;
         // one neighbour event: the W run up to col (and the row's own column if
@@ -1335,14 +1376,16 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
         // stream-ordered scratch: safe for concurrent calls on other streams
         const int q = 2 * p.n_sigma;
         const std::size_t bytes = static_cast<std::size_t>(q) * kPrefixCap * (sizeof(int) + 2 * sizeof(double)) +
-                                  static_cast<std::size_t>(q) * (2 * sizeof(int) + sizeof(double)) + 64;
+                                  static_cast<std::size_t>(q) * (2 * sizeof(int) + 2 * sizeof(double)) + 64;
         cudaError_t e = cudaMallocFromPoolAsync(&mem, bytes, static_cast<cudaMemPool_t>(pool), st);
         if (e != cudaSuccess) return e;
         char* b = static_cast<char*>(mem);
         T.s0 = reinterpret_cast<double*>(b);
         T.inc = T.s0 + q * kPrefixCap;
         T.s_end = T.inc + q * kPrefixCap;
-        T.t = reinterpret_cast<int*>(T.s_end + q);
+        T.iso = T.s_end + q;
+        T.iso_last = T.iso + q / 2;
+        T.t = reinterpret_cast<int*>(T.iso_last + q / 2);
         T.count = T.t + q * kPrefixCap;
         T.t_end = T.count + q;
         prefix_kernel<<<1, 64, 0, st>>>(p, T);
@@ -1426,8 +1469,12 @@ int launch_potentials(const PotentialLaunch& p, int kernel, void* pool, void* st
             case kUnit:
                 // a row range short of the whole graph is a shard of a
                 // multi-device sweep: hub rows walk whole (kLong)
-                if (ff && p.row_end - p.row_begin < p.n) launch(potential_warp_kernel<true, kUnit, true>);
-                else if (ff) launch(potential_warp_kernel<true, kUnit>);
+                if (ff && p.row_end - p.row_begin < p.n)
+                    p.iso ? launch(potential_warp_kernel<true, kUnit, true, true>)
+                          : launch(potential_warp_kernel<true, kUnit, true>);
+                else if (ff)
+                    p.iso ? launch(potential_warp_kernel<true, kUnit, false, true>)
+                          : launch(potential_warp_kernel<true, kUnit>);
                 else launch(potential_warp_kernel<false, kUnit>);
                 break;
             case kDevicePexp:
@@ -1710,14 +1757,56 @@ __host__ __device__ inline long long sample_row(int k, long long n) {
     h ^= h >> 29;
     return static_cast<long long>(h % static_cast<unsigned long long>(n));
 }
+// count[0]: sampled rows with <= kTinyRowDegree neighbours, count[1]: with none
 __global__ void tiny_sample_kernel(const long long* __restrict__ off, int n, int* __restrict__ count) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool tiny = k < kTinySample && off[sample_row(k, n) + 1] - off[sample_row(k, n)] <= kTinyRowDegree;
-    const unsigned m = __ballot_sync(0xffffffffu, tiny);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(count, __popc(m));
+    const long long d = k < kTinySample ? off[sample_row(k, n) + 1] - off[sample_row(k, n)] : 1 << 30;
+    const unsigned m = __ballot_sync(0xffffffffu, d <= kTinyRowDegree);
+    const unsigned z = __ballot_sync(0xffffffffu, d == 0);
+    if ((threadIdx.x & 31) == 0) {
+        if (m) atomicAdd(count, __popc(m));
+        if (z) atomicAdd(count + 1, __popc(z));
+    }
 }
 int sub_from_count(int tiny) { return 5 * tiny > kTinySample ? 16 : 32; }  // > 20% of rows tiny
+
+// The degree sample of a device CSR, cached per device and CSR pointer /
+// shape (one stream synchronisation the first time; only the speed depends
+// on it): {rows with <= 4 neighbours, isolated rows} among kTinySample.
+std::pair<int, int> degree_sample_device(const std::int64_t* offsets, int n, long long nnz, void* stream) {
+    if (n < 1) return {0, 0};
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, int, long long>, std::pair<int, int>> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_tuple(dev, static_cast<const void*>(offsets), n, nnz);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    auto st = static_cast<cudaStream_t>(stream);
+    int* d = nullptr;
+    int h[2] = {0, 0};
+    if (cudaMallocAsync(reinterpret_cast<void**>(&d), 2 * sizeof(int), st) != cudaSuccess) {
+        cudaGetLastError();
+        return {0, 0};
+    }
+    cudaMemsetAsync(d, 0, 2 * sizeof(int), st);
+    tiny_sample_kernel<<<kTinySample / kBlock, kBlock, 0, st>>>(reinterpret_cast<const long long*>(offsets), n, d);
+    count_launch();
+    cudaMemcpyAsync(h, d, 2 * sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(d, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return {0, 0};
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = {h[0], h[1]};
+    return {h[0], h[1]};
+}
 }  // namespace
+
+int isolated_rows_device(const std::int64_t* offsets, int n, long long nnz, void* stream) {
+    return 100 * degree_sample_device(offsets, n, nnz, stream).second > kTinySample ? 1 : 0;  // > 1% of rows
+}
 
 int light_row_sigmas_host(const std::int64_t* offsets, int n) {
     if (n < 1) return 32;
@@ -1730,34 +1819,7 @@ int light_row_sigmas_host(const std::int64_t* offsets, int n) {
 }
 
 int light_row_sigmas_device(const std::int64_t* offsets, int n, long long nnz, void* stream) {
-    if (n < 1) return 32;
-    static std::mutex mu;
-    static std::map<std::tuple<int, const void*, int, long long>, int> cache;  // per device, CSR shape
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const auto key = std::make_tuple(dev, static_cast<const void*>(offsets), n, nnz);
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        auto it = cache.find(key);
-        if (it != cache.end()) return it->second;
-    }
-    auto st = static_cast<cudaStream_t>(stream);
-    int* d = nullptr;
-    int h = 0;
-    if (cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(int), st) != cudaSuccess) {
-        cudaGetLastError();
-        return 32;
-    }
-    cudaMemsetAsync(d, 0, sizeof(int), st);
-    tiny_sample_kernel<<<kTinySample / kBlock, kBlock, 0, st>>>(reinterpret_cast<const long long*>(offsets), n, d);
-    count_launch();
-    cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st);
-    cudaFreeAsync(d, st);
-    if (cudaStreamSynchronize(st) != cudaSuccess) return 32;
-    const int sub = sub_from_count(h);
-    std::lock_guard<std::mutex> lk(mu);
-    cache[key] = sub;
-    return sub;
+    return sub_from_count(degree_sample_device(offsets, n, nnz, stream).first);
 }
 
 int launch_successors(int n, const std::int64_t* offsets, const std::int32_t* nbr, const double* v, int ld, int s0,
