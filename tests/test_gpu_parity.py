@@ -758,3 +758,23 @@ def test_sparse_graph_takes_16_sigma_argmin_launches_bitwise():
     assert np.array_equal(s_d.cpu().numpy(), succ)
     assert all(np.array_equal(ci_d[q].cpu().numpy(), res[q].cluster_index) for q in range(S))
     assert nc_d.cpu().tolist() == [r.num_clusters for r in res]
+
+
+@pytest.mark.parametrize("n", [6000, 6001])
+def test_isolated_rows_instantiation_bitwise(n):
+    """Graphs with isolated rows (> 1% of the degree sample) run the
+    fast-forward's isolated-row instantiation (numerator a per-sigma
+    constant): every potential equals the oracle's bit for bit, including
+    isolated rows at columns 0 and n - 1 under the odd-n Eigen tail."""
+    rng = np.random.default_rng(n)
+    m = n  # avg degree ~2: many isolated rows
+    u = rng.integers(1, n - 1, m).astype(np.int32)
+    v = rng.integers(1, n - 1, m).astype(np.int32)
+    keep = u != v
+    g = H.G(n, u[keep], v[keep], None, 10.0)  # rows 0 and n - 1 isolated
+    deg = np.diff(g.offsets)
+    assert deg[0] == 0 and deg[-1] == 0 and (deg == 0).mean() > 0.05
+    sig = O.log_sigma_grid(10.0, 32)
+    _, vg, _ = N.cluster_sweep(g.csr(N), sig, want_v=True)
+    for q in (0, 5, 11, 20, 31):
+        assert_bits(vg[q], O.potentials(g.offsets, g.nbr, g.wt, g.W, sig[q], workers=4))
