@@ -31,7 +31,7 @@ print(json.dumps({"median_ms": statistics.median(ts), "min_ms": min(ts)}))
 
 out = {}
 for wl in sys.argv[1:] or ["lfr"]:
-    for cuts in ["", "8,8,16", "4,8,8,12", "4,12,16", "8,24", "4,28", "16,8,8", "12,20"]:
+    for cuts in (os.environ["CUTS"].split(";") if os.environ.get("CUTS") else ["", "8,8,16", "4,8,8,12", "4,12,16", "8,24", "4,28", "16,8,8", "12,20"]):
         env = dict(os.environ)
         env.pop("GQC_GGD_CUTS", None)
         if cuts:
